@@ -1,0 +1,238 @@
+"""TEST INFRASTRUCTURE — ctypes binding to the CPU oracle (liblsnif_oracle.so).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu-baseline / reference
+leg may import this module, and only as the checker or the timed CPU
+reference. The product path (paper_2504_21627_b200) never imports it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PARITY_LIB = os.path.join(HERE, "liblsnif_oracle.so")
+FAST_LIB = os.path.join(HERE, "_native", "liblsnif_oracle_fast.so")
+
+RAY_DTYPE = np.dtype([("o", "<f4", 3), ("d", "<f4", 3), ("t_min", "<f4"), ("t_max", "<f4")])
+HIT_DTYPE = np.dtype([("flags_material", "<u4"), ("t_world", "<f4"), ("normal", "<f4", 3),
+                      ("albedo", "<f4", 3)])
+assert RAY_DTYPE.itemsize == 32 and HIT_DTYPE.itemsize == 32
+
+_P = C.c_void_p
+
+
+def build(fast: bool = False) -> str:
+    target = "fast" if fast else "all"
+    subprocess.run(["make", "-s", "-C", HERE, target], check=True)
+    return FAST_LIB if fast else PARITY_LIB
+
+
+def _load(path: str) -> C.CDLL:
+    lib = C.CDLL(path)
+    f = lib
+    f.oracle_last_error.restype = C.c_char_p
+    f.oracle_mix_bits.restype = C.c_uint64
+    f.oracle_mix_bits.argtypes = [C.c_uint64]
+    f.oracle_seed_stream.restype = C.c_uint32
+    f.oracle_seed_stream.argtypes = [C.c_uint64] * 4
+    f.oracle_float_to_half.restype = C.c_uint16
+    f.oracle_float_to_half.argtypes = [C.c_float]
+    f.oracle_half_to_float.restype = C.c_float
+    f.oracle_half_to_float.argtypes = [C.c_uint16]
+    f.oracle_hash_vertex.restype = C.c_uint32
+    f.oracle_hash_vertex.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint32]
+    f.oracle_ray_aabb.argtypes = [_P, _P, _P]
+    f.oracle_inflate_frame.argtypes = [_P, _P]
+    f.oracle_voxelize.argtypes = [_P, C.c_int, _P, C.c_int, _P, C.c_int, _P]
+    f.oracle_dda_local.argtypes = [_P, _P, C.c_float, C.c_float, _P, C.c_int, C.c_int, _P, _P,
+                                   _P, _P]
+    f.oracle_model_load.restype = _P
+    f.oracle_model_load.argtypes = [C.c_char_p]
+    f.oracle_model_free.argtypes = [_P]
+    f.oracle_model_save.argtypes = [_P, C.c_char_p]
+    f.oracle_model_info.argtypes = [_P, _P]
+    f.oracle_model_aabb.argtypes = [_P, _P]
+    f.oracle_model_occupancy.restype = _P
+    f.oracle_model_occupancy.argtypes = [_P]
+    f.oracle_model_random.restype = _P
+    f.oracle_model_random.argtypes = [_P, C.c_int, C.c_int, C.c_int, _P, C.c_int, C.c_uint32,
+                                      C.c_int, C.c_int, _P, C.c_uint64]
+    f.oracle_build_obj_model.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_uint64, C.c_char_p]
+    f.oracle_encode_point.argtypes = [_P, C.c_int, _P, C.c_int, _P, _P, _P, _P]
+    f.oracle_mlp_logits.argtypes = [_P, _P, _P]
+    f.oracle_infer_batch.argtypes = [_P, _P, C.c_int64, C.c_int64, _P, C.c_int64, _P]
+    f.oracle_narrow_phase.argtypes = [_P, _P, C.c_int64, C.c_int, _P, C.c_int]
+    f.oracle_time_narrow_phase.restype = C.c_double
+    f.oracle_time_narrow_phase.argtypes = [_P, _P, C.c_int64, C.c_int, _P, C.c_int, C.c_int]
+    f.oracle_trace.argtypes = [_P, _P, C.c_int64] + [_P] * 7
+    return lib
+
+
+_LIBS: dict[str, C.CDLL] = {}
+
+
+def lib(fast: bool = False) -> C.CDLL:
+    path = FAST_LIB if fast else PARITY_LIB
+    if path not in _LIBS:
+        if not os.path.exists(path):
+            build(fast)
+        _LIBS[path] = _load(path)
+    return _LIBS[path]
+
+
+def _ptr(a: np.ndarray) -> int:
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data
+
+
+def _check(st: int, L: C.CDLL) -> None:
+    if st == -1:
+        raise ValueError(L.oracle_last_error().decode())
+    if st < 0:
+        raise RuntimeError(L.oracle_last_error().decode())
+
+
+class OracleModel:
+    """A loaded LSNIF model inside the oracle (model_io.cpp:116-175)."""
+
+    def __init__(self, handle: int, fast: bool = False):
+        if not handle:
+            raise RuntimeError(lib(fast).oracle_last_error().decode())
+        self.h = handle
+        self.L = lib(fast)
+        info = np.zeros(9, np.int64)
+        self.L.oracle_model_info(self.h, _ptr(info))
+        (self.V, self.H, self.n_levels, self.F, self.M, self.hidden, self.n_mat,
+         *lv) = [int(v) for v in info]
+        self.level_res = lv[: self.n_levels]
+        self.aabb = np.zeros(6, np.float32)
+        self.L.oracle_model_aabb(self.h, _ptr(self.aabb))
+
+    @classmethod
+    def load(cls, path: str, fast: bool = False) -> "OracleModel":
+        return cls(lib(fast).oracle_model_load(path.encode()), fast)
+
+    @classmethod
+    def random(cls, occ: np.ndarray, V: int, H: int, levels, F: int, M: int, hidden: int,
+               n_mat: int, frame, seed: int) -> "OracleModel":
+        occ = np.ascontiguousarray(occ, np.uint8)
+        lv = np.ascontiguousarray(levels, np.int32)
+        fr = np.ascontiguousarray(frame, np.float32)
+        L = lib()
+        return cls(L.oracle_model_random(_ptr(occ), V, H, len(lv), _ptr(lv), F, M, hidden, n_mat,
+                                         _ptr(fr), seed))
+
+    def save(self, path: str) -> None:
+        _check(self.L.oracle_model_save(self.h, path.encode()), self.L)
+
+    @property
+    def input_width(self) -> int:
+        return self.H * self.n_levels * self.F
+
+    def occupancy(self) -> np.ndarray:
+        n = self.V ** 3 // 8
+        return np.ctypeslib.as_array(C.cast(self.L.oracle_model_occupancy(self.h),
+                                            C.POINTER(C.c_uint8)), (n,)).copy()
+
+    def narrow_phase(self, rays: np.ndarray, mode: int = 0, workers: int = 0) -> np.ndarray:
+        rays = np.ascontiguousarray(rays, RAY_DTYPE)
+        out = np.zeros(len(rays), HIT_DTYPE)
+        _check(self.L.oracle_narrow_phase(self.h, _ptr(rays), len(rays), mode, _ptr(out), workers),
+               self.L)
+        return out
+
+    def time_narrow_phase(self, rays: np.ndarray, mode: int = 0, workers: int = 0,
+                          reps: int = 3) -> float:
+        rays = np.ascontiguousarray(rays, RAY_DTYPE)
+        out = np.zeros(len(rays), HIT_DTYPE)
+        t = self.L.oracle_time_narrow_phase(self.h, _ptr(rays), len(rays), mode, _ptr(out),
+                                            workers, reps)
+        if t < 0:
+            _check(int(t), self.L)
+        return t
+
+    def trace(self, rays: np.ndarray) -> dict:
+        rays = np.ascontiguousarray(rays, RAY_DTYPE)
+        n, H, Lv, F = len(rays), self.H, self.n_levels, self.F
+        out = dict(info=np.zeros(n, np.int32), interval=np.zeros((n, 2), np.float32),
+                   t=np.zeros((n, H), np.float32), pts=np.zeros((n, H, 3), np.float32),
+                   cells=np.zeros((n, H), np.uint32), hidx=np.zeros((n, H, Lv, 8), np.uint32),
+                   feat=np.zeros((n, H * Lv * F), np.float32))
+        _check(self.L.oracle_trace(self.h, _ptr(rays), n, *[_ptr(out[k]) for k in
+                                   ("info", "interval", "t", "pts", "cells", "hidx", "feat")]),
+               self.L)
+        return out
+
+    def encode_point(self, level: int, p, volume: bool):
+        p = np.ascontiguousarray(p, np.float32)
+        feat = np.zeros(self.F, np.float32)
+        idx = np.zeros(8, np.uint32)
+        w = np.zeros(8, np.float32)
+        axis = C.c_int(0)
+        cnt = self.L.oracle_encode_point(self.h, level, _ptr(p), int(volume), _ptr(feat),
+                                         _ptr(idx), _ptr(w), C.addressof(axis))
+        return feat, idx[:cnt], w[:cnt], axis.value
+
+    def mlp_logits(self, x: np.ndarray) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float32)
+        z = np.zeros(8 + self.n_mat, np.float32)
+        self.L.oracle_mlp_logits(self.h, _ptr(x), _ptr(z))
+        return z
+
+    def infer_batch(self, inputs: np.ndarray, intervals: np.ndarray) -> np.ndarray:
+        """inputs: (n, input_width) — row j is column j of the reference's MatX."""
+        x = np.ascontiguousarray(inputs, np.float32)
+        iv = np.ascontiguousarray(intervals, np.float32).reshape(-1, 2)
+        out = np.zeros(len(x), HIT_DTYPE)
+        _check(self.L.oracle_infer_batch(self.h, _ptr(x), x.shape[1] if x.ndim == 2 else 0,
+                                         len(x), _ptr(iv), len(iv), _ptr(out)), self.L)
+        return out
+
+    def __del__(self):
+        try:
+            self.L.oracle_model_free(self.h)
+        except Exception:
+            pass
+
+
+def build_obj_model(obj_path: str, out_path: str, V: int = 32, H: int = 18, seed: int = 0) -> None:
+    L = lib()
+    _check(L.oracle_build_obj_model(obj_path.encode(), V, H, seed, out_path.encode()), L)
+
+
+def dda_local(o, d, t_min, t_max, occ: np.ndarray, res: int, cap: int):
+    L = lib()
+    o = np.ascontiguousarray(o, np.float32)
+    d = np.ascontiguousarray(d, np.float32)
+    occ = np.ascontiguousarray(occ, np.uint8)
+    pts = np.zeros((max(cap, 1), 3), np.float32)
+    t = np.zeros(max(cap, 1), np.float32)
+    cells = np.zeros((max(cap, 1), 3), np.int32)
+    fio = C.c_int(0)
+    n = L.oracle_dda_local(_ptr(o), _ptr(d), t_min, t_max, _ptr(occ), res, cap, _ptr(pts),
+                           _ptr(t), _ptr(cells), C.addressof(fio))
+    _check(min(n, 0), L)
+    return pts[:n], t[:n], cells[:n], bool(fio.value)
+
+
+def ray_aabb(ray, box):
+    L = lib()
+    r = np.zeros(1, RAY_DTYPE)
+    r["o"], r["d"], r["t_min"], r["t_max"] = ray
+    b = np.ascontiguousarray(box, np.float32)
+    out = np.zeros(2, np.float32)
+    ok = L.oracle_ray_aabb(_ptr(r), _ptr(b), _ptr(out))
+    return (float(out[0]), float(out[1])) if ok else None
+
+
+def voxelize(verts: np.ndarray, faces: np.ndarray, frame, res: int) -> np.ndarray:
+    L = lib()
+    v = np.ascontiguousarray(verts, np.float32)
+    f = np.ascontiguousarray(faces, np.int32)
+    fr = np.ascontiguousarray(frame, np.float32)
+    out = np.zeros(res ** 3 // 8, np.uint8)
+    _check(L.oracle_voxelize(_ptr(v), len(v), _ptr(f), len(f), _ptr(fr), res, _ptr(out)), L)
+    return out

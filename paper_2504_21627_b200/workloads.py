@@ -1,0 +1,131 @@
+"""Synthetic ray workloads for the LSNIF query path.
+
+All generators are index-addressable and deterministic, so every GPU rank can
+regenerate exactly its own shard, and the GPU path and the CPU oracle consume
+the same float32 ray file. Rays are the reference's `Ray` record
+(geometry.hpp:11-18), 32 B AoS: origin f32x3, direction f32x3, t_min, t_max.
+
+* camera rays: the reference pinhole camera (renderer.cpp:335-360) at pixel
+  centres (u = v = 0.5 instead of a random jitter);
+* incoherent rays: origins uniform in the model's frame box, directions
+  uniform on S^2 (sampling.hpp:26-31), drawn from a splitmix64 counter RNG
+  keyed by (seed, ray index) (types.hpp:25-39 mixing).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+RAY_DTYPE = np.dtype([("o", "<f4", 3), ("d", "<f4", 3), ("t_min", "<f4"), ("t_max", "<f4")])
+
+# C1/C2 framing of the teapot fixture.
+CAMERA = dict(position=(0.2505, 1.6, 4.5), look_at=(0.2505, 0.87, 0.0), up=(0.0, 1.0, 0.0),
+              vfov_deg=40.0)
+LIGHT = (3.0, 4.0, 3.0)
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _mix_bits(x: np.ndarray) -> np.ndarray:
+    """splitmix64 finalizer (types.hpp:25-31), vectorised over uint64."""
+    with np.errstate(over="ignore"):
+        x = x + np.uint64(0x9E3779B97F4A7C15)
+        x = (x ^ (x >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        x = (x ^ (x >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return x ^ (x >> np.uint64(31))
+
+
+def counter_uniforms(seed: int, index: np.ndarray, k: int) -> np.ndarray:
+    """k float32 uniforms in [0, 1) per index: 24-bit mantissas of
+    mix(mix(mix(seed + c) ^ index) ^ j)."""
+    with np.errstate(over="ignore"):
+        base = _mix_bits(np.uint64(seed) + np.uint64(0x632BE59BD9B4E019))
+        h = _mix_bits(base ^ index.astype(np.uint64))
+        out = np.empty((len(index), k), np.float32)
+        for j in range(k):
+            v = _mix_bits(h ^ np.uint64(j + 1))
+            out[:, j] = (v >> np.uint64(40)).astype(np.float32) * np.float32(1.0 / (1 << 24))
+    return out
+
+
+def camera_rays(width: int, height: int, rows: tuple[int, int] | None = None,
+                camera: dict = CAMERA) -> np.ndarray:
+    """Pixel-centre pinhole rays in row-major pixel order (renderer.cpp:346-360).
+    `rows` = (y0, y1) selects a row band (for tile sharding)."""
+    f32 = np.float32
+    pos = np.array(camera["position"], f32)
+    fwd = np.array(camera["look_at"], f32) - pos
+    fwd = fwd / np.sqrt(np.sum(fwd * fwd, dtype=f32))
+    up = np.array(camera["up"], f32)
+    right = np.cross(fwd, up).astype(f32)
+    right = right / np.sqrt(np.sum(right * right, dtype=f32))
+    upv = np.cross(right, fwd).astype(f32)
+    half_h = f32(math.tan(0.5 * camera["vfov_deg"] * math.pi / 180.0))
+    half_w = f32(half_h * f32(width) / f32(height))
+    y0, y1 = rows if rows is not None else (0, height)
+    py, px = np.meshgrid(np.arange(y0, y1, dtype=f32), np.arange(width, dtype=f32), indexing="ij")
+    sx = (f32(2) * (px + f32(0.5)) / f32(width) - f32(1)).reshape(-1, 1)
+    sy = (f32(1) - f32(2) * (py + f32(0.5)) / f32(height)).reshape(-1, 1)
+    d = fwd + (sx * half_w) * right + (sy * half_h) * upv
+    d = d / np.sqrt(np.sum(d * d, axis=1, keepdims=True, dtype=f32))
+    rays = np.zeros(len(d), RAY_DTYPE)
+    rays["o"] = pos
+    rays["d"] = d.astype(f32)
+    rays["t_min"] = 0.0
+    rays["t_max"] = np.inf
+    return rays
+
+
+def incoherent_rays(n: int, box: np.ndarray, seed: int = 3, start: int = 0) -> np.ndarray:
+    """C3/C5 rays [start, start+n): origin uniform in `box` (min xyz, max xyz),
+    direction uniform on the sphere (sampling.hpp:26-31)."""
+    f32 = np.float32
+    box = np.asarray(box, f32)
+    idx = np.arange(start, start + n, dtype=np.uint64)
+    u = counter_uniforms(seed, idx, 5)
+    mn, mx = box[:3], box[3:]
+    o = mn + u[:, :3] * (mx - mn)
+    z = f32(1) - f32(2) * u[:, 3]
+    r = np.sqrt(np.maximum(f32(0), f32(1) - z * z))
+    phi = f32(2 * math.pi) * u[:, 4]
+    rays = np.zeros(n, RAY_DTYPE)
+    rays["o"] = o
+    rays["d"] = np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=1).astype(f32)
+    rays["t_min"] = 0.0
+    rays["t_max"] = np.inf
+    return rays
+
+
+def shadow_rays(primary: np.ndarray, hits: np.ndarray, box: np.ndarray,
+                light=LIGHT, eps_scale: float = 1e-3) -> tuple[np.ndarray, np.ndarray]:
+    """One NEE shadow ray per accepted neural hit (renderer.cpp:384-427 at
+    identity transform, diffuse material, one point light): spawn at
+    hit + eps*n with eps = 1e-3 * frame diagonal, normal from the head (or -d
+    when zero) flipped to face the ray, kept iff n.wi > 0, t_max = 0.9999*dist.
+    Returns (rays, owner index)."""
+    f32 = np.float32
+    acc = (hits["flags_material"] & 4) != 0
+    idx = np.nonzero(acc)[0]
+    o = primary["o"][idx]
+    d = primary["d"][idx]
+    t = hits["t_world"][idx].reshape(-1, 1)
+    pos = o + t * d
+    n = hits["normal"][idx].astype(f32)
+    zero = np.sum(n * n, axis=1) == 0
+    n[zero] = -d[zero]
+    flip = np.sum(n * d, axis=1) > 0
+    n[flip] = -n[flip]
+    box = np.asarray(box, f32)
+    diag = f32(np.sqrt(np.sum((box[3:] - box[:3]) ** 2)))
+    spawn = pos + f32(eps_scale) * diag * n
+    to_l = np.asarray(light, f32) - spawn
+    dist = np.sqrt(np.sum(to_l * to_l, axis=1))
+    wi = to_l / dist.reshape(-1, 1)
+    keep = (np.sum(n * wi, axis=1) > 0) & (dist > 0)
+    rays = np.zeros(int(keep.sum()), RAY_DTYPE)
+    rays["o"] = spawn[keep]
+    rays["d"] = wi[keep]
+    rays["t_min"] = 0.0
+    rays["t_max"] = dist[keep] * f32(1 - 1e-4)
+    return rays, idx[keep]
