@@ -1,0 +1,23 @@
+# Builds liblsnif_gpu.so (sm_100a) in-tree, and the CPU oracle (test infra).
+NVCC ?= /usr/local/cuda/bin/nvcc
+PKG := paper_2504_21627_b200
+SRC := $(PKG)/csrc/lsnif_kernels.cu $(PKG)/csrc/lsnif_capi.cu
+HDR := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.hpp) include/lsnif_gpu.h
+NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+           -Xcompiler -fPIC -Xcompiler -ffp-contract=off -Xptxas -v \
+           -Iinclude -I$(PKG)/csrc
+
+all: $(PKG)/liblsnif_gpu.so oracle
+
+$(PKG)/liblsnif_gpu.so: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> build_ptxas.log || (cat build_ptxas.log; false)
+	@grep -E "registers|spill|error" build_ptxas.log | sed 's/^ptxas info    ://' | head -40
+
+oracle:
+	$(MAKE) -s -C oracle all
+
+clean:
+	rm -f $(PKG)/liblsnif_gpu.so build_ptxas.log
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle clean

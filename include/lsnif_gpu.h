@@ -1,0 +1,176 @@
+/*
+ * lsnif_gpu.h — C ABI of the B200-native LSNIF batched ray-query path.
+ *
+ * This is the drop-in boundary for the reference's narrow phase. The
+ * reference has no plugin/FFI layer; its query surface is the C++ API in
+ * proj/include/lsnif/renderer.hpp and the file-local driver
+ * run_narrow_phase (proj/src/renderer.cpp:232-265). Each entry point below
+ * names the reference interface it replaces. Plain pointers and sizes only;
+ * CUDA streams are passed as `void*` (a cudaStream_t, NULL = legacy stream).
+ *
+ * Threading: every call is reentrant. Calls on distinct streams may run
+ * concurrently (per-stream scratch); a model is read-only after creation
+ * (reference: shared_ptr<const LsnifModel>, renderer.hpp:76).
+ * Errors: a non-zero lsnif_status plus a thread-local message
+ * (lsnif_last_error). LSNIF_INVALID_ARGUMENT corresponds to the reference's
+ * std::invalid_argument (renderer.cpp:185-189), LSNIF_RUNTIME_ERROR to
+ * std::runtime_error (model_io.cpp:118-141).
+ */
+#ifndef LSNIF_GPU_H_
+#define LSNIF_GPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum lsnif_status {
+  LSNIF_OK = 0,
+  LSNIF_INVALID_ARGUMENT = 1,
+  LSNIF_RUNTIME_ERROR = 2,
+  LSNIF_CUDA_ERROR = 3,
+  LSNIF_UNSUPPORTED = 4
+} lsnif_status;
+
+/* lsnif::Ray (geometry.hpp:11-18), object space of the model, 32 B. */
+typedef struct lsnif_ray {
+  float origin[3];
+  float direction[3];
+  float t_min;
+  float t_max;
+} lsnif_ray;
+
+/* lsnif::RayInterval (geometry.hpp:47-50). */
+typedef struct lsnif_interval {
+  float enter;
+  float exit;
+} lsnif_interval;
+
+/* One query result, 32 B. Carries lsnif::NeuralHit (renderer.hpp:42-48)
+ * plus the pipeline flags around it:
+ *   bit 0 PAIR      the ray overlaps the model's frame box before t_max
+ *                   (pair emission, renderer.cpp:165-172);
+ *   bit 1 OCCLUDED  NeuralHit::occluded (sigmoid(z0) > 0.5, renderer.cpp:212);
+ *   bit 2 ACCEPTED  the closest-hit (renderer.cpp:281-284) or any-hit
+ *                   (renderer.cpp:317-320) accept rule holds;
+ *   bits 8..31      NeuralHit::material_index.
+ * t_world / normal / albedo are NeuralHit's fields (valid when PAIR). */
+typedef struct lsnif_hit {
+  uint32_t flags_material;
+  float t_world;
+  float normal[3];
+  float albedo[3];
+} lsnif_hit;
+
+#define LSNIF_HIT_PAIR 1u
+#define LSNIF_HIT_OCCLUDED 2u
+#define LSNIF_HIT_ACCEPTED 4u
+#define LSNIF_HIT_MATERIAL_SHIFT 8
+
+/* lsnif::Material (geometry.hpp:56-60), as stored in the model file. */
+typedef struct lsnif_material {
+  float albedo[3];
+  uint32_t kind; /* 0 diffuse, 1 glossy */
+  float roughness;
+} lsnif_material;
+
+/* Host-side mirror of lsnif::LsnifModel (model_io.hpp:18-36) with the
+ * binary16 payloads exactly as in the LSNF v1 file (model_io.hpp:38-43). */
+typedef struct lsnif_model_desc {
+  int32_t voxel_res;  /* V */
+  int32_t hit_cap;    /* H */
+  int32_t n_levels;   /* L */
+  int32_t f_dim;      /* F */
+  uint32_t table_size; /* M */
+  int32_t hidden;
+  int32_t n_mat;
+  const uint8_t* occupancy;        /* V^3/8 bytes, x fastest (voxel.hpp:10-11) */
+  const int32_t* level_res;        /* n_levels */
+  const uint16_t* const* tables;   /* n_levels x (M*F binary16, entry-major) */
+  const uint16_t* w1;              /* hidden x (H*L*F), row-major binary16 */
+  const uint16_t* b1;
+  const uint16_t* w2;              /* hidden x hidden */
+  const uint16_t* b2;
+  const uint16_t* w3;              /* (8+n_mat) x hidden */
+  const uint16_t* b3;
+  const lsnif_material* materials;
+  int32_t n_materials;
+  float aabb[6];                   /* inflated frame box: min xyz, max xyz */
+} lsnif_model_desc;
+
+typedef struct lsnif_model_info {
+  int32_t voxel_res, hit_cap, n_levels, f_dim;
+  uint32_t table_size;
+  int32_t hidden, n_mat, n_materials;
+  int32_t level_res[4];
+  float aabb[6];
+  float activation_scale; /* power-of-two fp16 operand scale */
+  uint64_t device_bytes;
+} lsnif_model_info;
+
+/* Counters of the last lsnif_query on a stream (filled when requested). */
+typedef struct lsnif_query_stats {
+  int64_t rays;        /* queries answered */
+  int64_t pairs;       /* rays overlapping the frame box */
+  int64_t mlp_rows;    /* pairs with >= 1 boundary point (run through the MLP) */
+  int64_t points;      /* boundary points encoded */
+  int64_t volume_points;
+} lsnif_query_stats;
+
+typedef struct lsnif_model_s* lsnif_model;
+
+enum { LSNIF_QUERY_CLOSEST = 0, LSNIF_QUERY_ANY = 1 };
+
+/* Replaces load_model (model_io.cpp:116-175) + the model upload done once per
+ * object in PreparedScene::prepare (renderer.cpp:55-76). */
+lsnif_status lsnif_model_load(const char* path, int device, lsnif_model* out);
+/* Same, from host arrays mirroring LsnifModel. */
+lsnif_status lsnif_model_create(const lsnif_model_desc* desc, int device, lsnif_model* out);
+lsnif_status lsnif_model_destroy(lsnif_model model);
+lsnif_status lsnif_model_get_info(lsnif_model model, lsnif_model_info* out);
+
+/* Replaces run_narrow_phase (renderer.cpp:232-265) for one object group,
+ * fused with pair emission (renderer.cpp:165-172) and the accept rule of
+ * intersect_scene (mode CLOSEST, renderer.cpp:280-301) or occluded_batch
+ * (mode ANY, renderer.cpp:316-321). Rays/hits are DEVICE pointers; one
+ * result per ray, in ray order. Asynchronous on `stream`. */
+lsnif_status lsnif_query(lsnif_model model, const lsnif_ray* d_rays, int64_t n, int mode,
+                         lsnif_hit* d_hits, void* stream);
+
+/* Same with HOST rays/hits (pinned or pageable): chunked H2D / query / D2H,
+ * overlapped on internal streams. Synchronous. */
+lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_t n, int mode,
+                              lsnif_hit* h_hits, void* stream);
+
+/* Replaces infer_batch (renderer.cpp:183-226): `inputs` is the reference's
+ * MatX inputs(input_width, n) column-major fp32 (DEVICE), intervals n
+ * entries (DEVICE). Throws-equivalent LSNIF_INVALID_ARGUMENT when
+ * n != n_intervals or rows != input_width. Results carry OCCLUDED and the
+ * NeuralHit fields; PAIR/ACCEPTED are not set. */
+lsnif_status lsnif_infer_batch(lsnif_model model, const float* d_inputs, int64_t rows, int64_t n,
+                               const lsnif_interval* d_intervals, int64_t n_intervals,
+                               lsnif_hit* d_hits, void* stream);
+
+/* Bit-exactness probe: per-ray pair/interval, DDA boundary points, t
+ * values, cells, hash indices and fp32 features, produced by the same device
+ * functions the query kernels use. DEVICE output arrays (H/L/F of the model):
+ *   info[n] (count | first_is_origin<<8 | pair<<9), interval[n][2], t[n][H],
+ *   pts[n][H][3], cells[n][H] (x | y<<8 | z<<16), hidx[n][H][L][8],
+ *   feat[n][H*L*F]. */
+lsnif_status lsnif_debug_traverse(lsnif_model model, const lsnif_ray* d_rays, int64_t n,
+                                  int32_t* info, float* interval, float* t, float* pts,
+                                  uint32_t* cells, uint32_t* hidx, float* feat, void* stream);
+
+/* Counters of the most recent lsnif_query on `stream` (synchronises it). */
+lsnif_status lsnif_last_query_stats(lsnif_model model, void* stream, lsnif_query_stats* out);
+
+const char* lsnif_last_error(void);
+const char* lsnif_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LSNIF_GPU_H_ */

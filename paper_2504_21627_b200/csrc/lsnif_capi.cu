@@ -1,0 +1,670 @@
+// C ABI of liblsnif_gpu (include/lsnif_gpu.h): model ingest and device
+// residency, per-stream scratch, query orchestration, host staging.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lsnif_gpu.h"
+#include "lsnif_internal.hpp"
+
+using lsnif_dev::DevModel;
+using lsnif_dev::RowMeta;
+using lsnif_dev::kTileM;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct ApiError {
+  lsnif_status st;
+  std::string msg;
+};
+
+[[noreturn]] void fail(lsnif_status st, const std::string& msg) { throw ApiError{st, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(LSNIF_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <typename F>
+lsnif_status guarded(F&& f) {
+  try {
+    f();
+    return LSNIF_OK;
+  } catch (const ApiError& e) {
+    g_err = e.msg;
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return LSNIF_RUNTIME_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return LSNIF_RUNTIME_ERROR;
+  }
+}
+
+// ------------------------------------------------------------ fp16 decode
+float half_bits_to_float(uint16_t h) {  // IEEE binary16 -> fp32 (exact)
+  const uint32_t sign = static_cast<uint32_t>(h & 0x8000u) << 16;
+  const uint32_t exp = (h >> 10) & 0x1fu;
+  uint32_t man = h & 0x3ffu;
+  uint32_t x;
+  if (exp == 0) {
+    if (man == 0) {
+      x = sign;
+    } else {
+      int shift = 0;
+      while (!(man & 0x400u)) {
+        man <<= 1;
+        ++shift;
+      }
+      man &= 0x3ffu;
+      x = sign | static_cast<uint32_t>(113 - shift) << 23 | (man << 13);
+    }
+  } else if (exp == 31) {
+    x = sign | 0x7f800000u | (man << 13);
+  } else {
+    x = sign | ((exp - 15 + 127) << 23) | (man << 13);
+  }
+  float f;
+  std::memcpy(&f, &x, 4);
+  return f;
+}
+
+uint16_t float_to_half_bits(float v) {  // exact for the powers of two used here
+  const __half h = __float2half_rn(v);
+  uint16_t b;
+  std::memcpy(&b, &h, 2);
+  return b;
+}
+
+// ------------------------------------------------------------- workspace
+struct Workspace {
+  uint8_t* X = nullptr;
+  size_t x_tiles = 0;
+  RowMeta* meta = nullptr;
+  size_t meta_cap = 0;
+  int32_t* counter = nullptr;
+  unsigned long long* stats = nullptr;
+  int64_t last_rays = 0;
+  ~Workspace() {
+    cudaFree(X);
+    cudaFree(meta);
+    cudaFree(counter);
+    cudaFree(stats);
+  }
+};
+
+struct HostStaging {
+  cudaStream_t streams[2] = {nullptr, nullptr};
+  lsnif_ray* d_rays[2] = {nullptr, nullptr};
+  lsnif_hit* d_hits[2] = {nullptr, nullptr};
+  int64_t cap = 0;
+  ~HostStaging() {
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(d_rays[i]);
+      cudaFree(d_hits[i]);
+      if (streams[i]) cudaStreamDestroy(streams[i]);
+    }
+  }
+};
+
+constexpr int64_t kChunk = int64_t(1) << 21;      // rays per trace/MLP launch pair
+constexpr int64_t kHostChunk = int64_t(1) << 20;  // rays per host staging step
+
+}  // namespace
+
+struct lsnif_model_s {
+  int device = 0;
+  int num_sms = 148;
+  DevModel dm{};
+  lsnif_model_info info{};
+  std::vector<void*> allocations;
+  std::mutex mu;
+  std::map<cudaStream_t, std::unique_ptr<Workspace>> ws;
+  std::unique_ptr<HostStaging> staging;
+  std::mutex staging_mu;
+
+  ~lsnif_model_s() {
+    cudaSetDevice(device);
+    ws.clear();
+    staging.reset();
+    for (void* p : allocations) cudaFree(p);
+  }
+
+  template <typename T>
+  T* upload(const void* src, size_t bytes) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, bytes), "cudaMalloc(model)");
+    allocations.push_back(p);
+    ck(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice), "cudaMemcpy(model)");
+    info.device_bytes += bytes;
+    return static_cast<T*>(p);
+  }
+
+  Workspace& workspace(cudaStream_t st, int64_t n) {
+    std::lock_guard<std::mutex> lock(mu);
+    auto& slot = ws[st];
+    if (!slot) {
+      slot = std::make_unique<Workspace>();
+      ck(cudaMalloc(&slot->counter, 64), "cudaMalloc(counter)");
+      ck(cudaMalloc(&slot->stats, 64), "cudaMalloc(stats)");
+    }
+    Workspace& w = *slot;
+    const int64_t rows = std::min<int64_t>(n, kChunk);
+    const size_t tiles = static_cast<size_t>((rows + kTileM - 1) / kTileM);
+    if (tiles > w.x_tiles) {
+      cudaFree(w.X);
+      w.X = nullptr;
+      ck(cudaMalloc(&w.X, tiles * tile_bytes()), "cudaMalloc(X)");
+      w.x_tiles = tiles;
+    }
+    if (static_cast<size_t>(rows) > w.meta_cap) {
+      cudaFree(w.meta);
+      w.meta = nullptr;
+      ck(cudaMalloc(&w.meta, static_cast<size_t>(rows) * sizeof(RowMeta)), "cudaMalloc(meta)");
+      w.meta_cap = static_cast<size_t>(rows);
+    }
+    return w;
+  }
+
+  uint32_t tile_bytes() const { return static_cast<uint32_t>(kTileM) * dm.K1P * 2; }
+};
+
+namespace {
+
+// Builds the device model from a host description (model_io.hpp:18-36).
+void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
+  const int V = d.voxel_res, H = d.hit_cap, L = d.n_levels, F = d.f_dim, hid = d.hidden;
+  if (V < 2 || V > 256 || (V & (V - 1)) != 0)
+    fail(LSNIF_INVALID_ARGUMENT, "occupancy resolution must be a power of two in [2, 256]");
+  if (H < 1) fail(LSNIF_INVALID_ARGUMENT, "hit cap must be >= 1");
+  if (L < 1) fail(LSNIF_INVALID_ARGUMENT, "need at least one grid level");
+  if (d.n_mat < 1) fail(LSNIF_INVALID_ARGUMENT, "n_mat must be >= 1");
+  if (d.table_size < 1) fail(LSNIF_INVALID_ARGUMENT, "table size must be >= 1");
+  for (int l = 0; l < L; ++l)
+    if (d.level_res[l] % V != 0)
+      fail(LSNIF_INVALID_ARGUMENT, "level resolution must be a multiple of the voxel resolution");
+  // Fast-path envelope of this build.
+  if (V > 64) fail(LSNIF_UNSUPPORTED, "voxel resolution > 64 is not supported by the GPU path");
+  if (H > lsnif_dev::kMaxHitCap) fail(LSNIF_UNSUPPORTED, "hit cap > 32 is not supported");
+  if (L > lsnif_dev::kMaxLevels || F > 4 || L * F > 16)
+    fail(LSNIF_UNSUPPORTED, "need n_levels <= 4, f_dim <= 4, n_levels * f_dim <= 16");
+  if (hid != 64 && hid != 128) fail(LSNIF_UNSUPPORTED, "hidden width must be 64 or 128");
+  const int n_out = 8 + d.n_mat;
+  if (n_out > 16) fail(LSNIF_UNSUPPORTED, "n_mat > 8 is not supported");
+  const int K1 = H * L * F;
+  const int K1P = (K1 + 1 + 15) / 16 * 16;
+  if (K1P > hid + 16) fail(LSNIF_UNSUPPORTED, "input width H*L*F must be < hidden + 16");
+
+  DevModel& m = M.dm;
+  m = DevModel{};
+  for (int a = 0; a < 3; ++a) {
+    m.mn[a] = d.aabb[a];
+    m.mx[a] = d.aabb[3 + a];
+    m.inv_ext[a] = 1.0f / (m.mx[a] - m.mn[a]);  // model_io.hpp:33 cwiseInverse
+  }
+  m.V = V;
+  m.fres = static_cast<float>(V);
+  m.inv_fres = 1.0f / static_cast<float>(V);
+  m.H = H;
+  m.L = L;
+  m.F = F;
+  m.LF = L * F;
+  m.K1 = K1;
+  m.K1P = K1P;
+  m.M = d.table_size;
+  m.M_pow2 = (d.table_size & (d.table_size - 1)) == 0;
+  m.M_mask = d.table_size - 1;
+  for (int l = 0; l < L; ++l) m.level_res[l] = d.level_res[l];
+  m.hidden = hid;
+  m.n_out = n_out;
+  m.n_mat = d.n_mat;
+  m.N3 = 16;
+
+  // occupancy bitset as 32-bit words (same bit order as the byte stream)
+  const size_t occ_bytes = static_cast<size_t>(V) * V * V / 8;
+  std::vector<uint32_t> occ((occ_bytes + 3) / 4, 0u);
+  std::memcpy(occ.data(), d.occupancy, occ_bytes);
+  m.occ = M.upload<uint32_t>(occ.data(), occ.size() * 4);
+
+  // hash tables: 4 binary16 per entry (8 B, one load per corner)
+  float xmax = 0.0f;
+  for (int l = 0; l < L; ++l) {
+    std::vector<uint16_t> t(static_cast<size_t>(d.table_size) * 4, 0);
+    for (uint32_t e = 0; e < d.table_size; ++e)
+      for (int f = 0; f < F; ++f) {
+        const uint16_t h = d.tables[l][static_cast<size_t>(e) * F + f];
+        t[static_cast<size_t>(e) * 4 + f] = h;
+        xmax = std::max(xmax, std::fabs(half_bits_to_float(h)));
+      }
+    m.tables[l] = M.upload<uint2>(t.data(), t.size() * 2);
+  }
+
+  // decoded fp32 weights (row-major) for the fp32 infer_batch kernel + bounds
+  auto dec = [](const uint16_t* src, size_t n) {
+    std::vector<float> v(n);
+    for (size_t i = 0; i < n; ++i) v[i] = half_bits_to_float(src[i]);
+    return v;
+  };
+  const std::vector<float> w1 = dec(d.w1, static_cast<size_t>(hid) * K1), b1 = dec(d.b1, hid);
+  const std::vector<float> w2 = dec(d.w2, static_cast<size_t>(hid) * hid), b2 = dec(d.b2, hid);
+  const std::vector<float> w3 = dec(d.w3, static_cast<size_t>(n_out) * hid), b3 = dec(d.b3, n_out);
+  {
+    std::vector<float> all;
+    for (const auto* v : {&w1, &b1, &w2, &b2, &w3, &b3}) all.insert(all.end(), v->begin(), v->end());
+    m.w_f32 = M.upload<float>(all.data(), all.size() * 4);
+  }
+
+  // Activation scale: a power of two s with s * |activation| <= 2^14 for
+  // every fp16 operand, from rigorous bounds (|feature| <= max|entry|,
+  // |z_i| <= sum_j |W_ij| * bound + |b_i|).
+  auto layer_bound = [](const std::vector<float>& w, const std::vector<float>& b, int rows, int cols,
+                        double in_bound) {
+    double mx = 0.0;
+    for (int i = 0; i < rows; ++i) {
+      double s = std::fabs(b[static_cast<size_t>(i)]);
+      for (int j = 0; j < cols; ++j) s += std::fabs(w[static_cast<size_t>(i) * cols + j]) * in_bound;
+      mx = std::max(mx, s);
+    }
+    return mx;
+  };
+  const double B1 = layer_bound(w1, b1, hid, K1, xmax);
+  const double B2 = layer_bound(w2, b2, hid, hid, B1);
+  const double B3 = layer_bound(w3, b3, n_out, hid, B2);
+  const double bmax = std::max({static_cast<double>(xmax), B1, B2, B3, 1e-30});
+  int e = static_cast<int>(std::floor(std::log2(16384.0 / bmax)));
+  e = std::max(-14, std::min(15, e));
+  m.act_scale = std::ldexp(1.0f, e);
+  m.inv_act_scale = std::ldexp(1.0f, -e);
+  M.info.activation_scale = m.act_scale;
+
+  // UMMA canonical fp16 operands with the bias folded in as column K:
+  //   W1: hid x K1P (col K1 = b1), W2: hid x (hid+16) (col hid = b2),
+  //   W3: 16 x (hid+16) (col hid = b3, rows >= n_out zero).
+  const int K2 = hid + 16;
+  auto canon = [&](int rows, int cols, auto&& get) {
+    std::vector<uint8_t> buf(static_cast<size_t>(rows) * cols * 2, 0);
+    for (int r = 0; r < rows; ++r)
+      for (int c = 0; c < cols; ++c) {
+        const uint16_t h = get(r, c);
+        std::memcpy(buf.data() + lsnif_dev::canon_offset(r, c, rows), &h, 2);
+      }
+    return buf;
+  };
+  const auto c1 = canon(hid, K1P, [&](int r, int c) -> uint16_t {
+    if (c < K1) return d.w1[static_cast<size_t>(r) * K1 + c];
+    return c == K1 ? d.b1[r] : uint16_t(0);
+  });
+  const auto c2 = canon(hid, K2, [&](int r, int c) -> uint16_t {
+    if (c < hid) return d.w2[static_cast<size_t>(r) * hid + c];
+    return c == hid ? d.b2[r] : uint16_t(0);
+  });
+  const auto c3 = canon(16, K2, [&](int r, int c) -> uint16_t {
+    if (r >= n_out) return 0;
+    if (c < hid) return d.w3[static_cast<size_t>(r) * hid + c];
+    return c == hid ? d.b3[r] : uint16_t(0);
+  });
+  std::vector<uint8_t> wc;
+  wc.insert(wc.end(), c1.begin(), c1.end());
+  wc.insert(wc.end(), c2.begin(), c2.end());
+  wc.insert(wc.end(), c3.begin(), c3.end());
+  m.w_canon = M.upload<uint8_t>(wc.data(), wc.size());
+  m.w1_bytes = static_cast<uint32_t>(c1.size());
+  m.w2_bytes = static_cast<uint32_t>(c2.size());
+  m.w3_bytes = static_cast<uint32_t>(c3.size());
+
+  // Logits of the all-zero input (rays without boundary points), fp32 with
+  // the reference's sequential order (renderer.cpp:197-207).
+  {
+    std::vector<float> h1(hid), h2(hid);
+    for (int i = 0; i < hid; ++i) {
+      float s = 0.0f;
+      for (int j = 0; j < K1; ++j) s += w1[static_cast<size_t>(i) * K1 + j] * 0.0f;
+      s = s + b1[i];
+      h1[i] = s < 0.0f ? s * 0.01f : s;
+    }
+    for (int i = 0; i < hid; ++i) {
+      float s = 0.0f;
+      for (int j = 0; j < hid; ++j) {
+        const float p = w2[static_cast<size_t>(i) * hid + j] * h1[j];
+        s = s + p;
+      }
+      s = s + b2[i];
+      h2[i] = s < 0.0f ? s * 0.01f : s;
+    }
+    for (int i = 0; i < n_out; ++i) {
+      float s = 0.0f;
+      for (int j = 0; j < hid; ++j) {
+        const float p = w3[static_cast<size_t>(i) * hid + j] * h2[j];
+        s = s + p;
+      }
+      m.z_zero[i] = s + b3[i];
+    }
+  }
+
+  M.info.voxel_res = V;
+  M.info.hit_cap = H;
+  M.info.n_levels = L;
+  M.info.f_dim = F;
+  M.info.table_size = d.table_size;
+  M.info.hidden = hid;
+  M.info.n_mat = d.n_mat;
+  M.info.n_materials = d.n_materials;
+  for (int l = 0; l < L && l < 4; ++l) M.info.level_res[l] = d.level_res[l];
+  for (int a = 0; a < 6; ++a) M.info.aabb[a] = d.aabb[a];
+}
+
+// LSNF v1 reader (model_io.cpp:116-175): same checks and messages.
+struct FileModel {
+  lsnif_model_desc desc{};
+  std::vector<uint8_t> occ;
+  std::vector<int32_t> levels;
+  std::vector<std::vector<uint16_t>> tables;
+  std::vector<const uint16_t*> table_ptrs;
+  std::vector<uint16_t> w1, b1, w2, b2, w3, b3;
+  std::vector<lsnif_material> materials;
+};
+
+void read_model_file(const std::string& path, FileModel& fm) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) fail(LSNIF_RUNTIME_ERROR, "cannot open model file: " + path);
+  auto rd = [&](void* dst, size_t n) {
+    if (!in.read(static_cast<char*>(dst), static_cast<std::streamsize>(n)))
+      fail(LSNIF_RUNTIME_ERROR, "model file truncated");
+  };
+  auto u32 = [&]() {
+    uint32_t v;
+    rd(&v, 4);
+    return v;
+  };
+  char magic[4];
+  rd(magic, 4);
+  if (std::memcmp(magic, "LSNF", 4) != 0)
+    fail(LSNIF_RUNTIME_ERROR, "not an LSNIF model file (bad magic): " + path);
+  const uint32_t version = u32();
+  if (version != 1u) fail(LSNIF_RUNTIME_ERROR, "unsupported model version " + std::to_string(version));
+  lsnif_model_desc& d = fm.desc;
+  d.voxel_res = static_cast<int32_t>(u32());
+  d.hit_cap = static_cast<int32_t>(u32());
+  d.n_levels = static_cast<int32_t>(u32());
+  d.f_dim = static_cast<int32_t>(u32());
+  d.table_size = u32();
+  d.hidden = static_cast<int32_t>(u32());
+  d.n_mat = static_cast<int32_t>(u32());
+  const int V = d.voxel_res;
+  if (V < 2 || V > 256 || (V & (V - 1)) != 0)
+    fail(LSNIF_INVALID_ARGUMENT, "occupancy resolution must be a power of two in [2, 256]");
+  if (d.n_levels < 1 || d.n_levels > 64 || d.f_dim < 1 || d.f_dim > 64 || d.hidden < 1 ||
+      d.hidden > 4096 || d.n_mat < 1 || d.n_mat > 4096 || d.hit_cap < 1 || d.hit_cap > 4096)
+    fail(LSNIF_RUNTIME_ERROR, "model header out of range: " + path);
+  fm.occ.resize(static_cast<size_t>(V) * V * V / 8);
+  rd(fm.occ.data(), fm.occ.size());
+  for (int l = 0; l < d.n_levels; ++l) {
+    fm.levels.push_back(static_cast<int32_t>(u32()));
+    std::vector<uint16_t> t(static_cast<size_t>(d.table_size) * d.f_dim);
+    rd(t.data(), t.size() * 2);
+    fm.tables.push_back(std::move(t));
+  }
+  const size_t K1 = static_cast<size_t>(d.hit_cap) * d.n_levels * d.f_dim;
+  const size_t hid = static_cast<size_t>(d.hidden), no = 8 + static_cast<size_t>(d.n_mat);
+  auto vec = [&](std::vector<uint16_t>& v, size_t n) {
+    v.resize(n);
+    rd(v.data(), n * 2);
+  };
+  vec(fm.w1, hid * K1);
+  vec(fm.b1, hid);
+  vec(fm.w2, hid * hid);
+  vec(fm.b2, hid);
+  vec(fm.w3, no * hid);
+  vec(fm.b3, no);
+  const uint32_t nm = u32();
+  if (nm > 1u << 20) fail(LSNIF_RUNTIME_ERROR, "model file truncated");
+  fm.materials.resize(nm);
+  for (auto& mt : fm.materials) {
+    rd(mt.albedo, 12);
+    mt.kind = u32() == 1u ? 1u : 0u;
+    rd(&mt.roughness, 4);
+  }
+  rd(d.aabb, 24);
+  for (auto& t : fm.tables) fm.table_ptrs.push_back(t.data());
+  d.occupancy = fm.occ.data();
+  d.level_res = fm.levels.data();
+  d.tables = fm.table_ptrs.data();
+  d.w1 = fm.w1.data();
+  d.b1 = fm.b1.data();
+  d.w2 = fm.w2.data();
+  d.b2 = fm.b2.data();
+  d.w3 = fm.w3.data();
+  d.b3 = fm.b3.data();
+  d.materials = fm.materials.data();
+  d.n_materials = static_cast<int32_t>(nm);
+}
+
+void check_model(lsnif_model m) {
+  if (!m) fail(LSNIF_INVALID_ARGUMENT, "null model");
+}
+
+void create_into(const lsnif_model_desc& d, int device, lsnif_model* out) {
+  if (!out) fail(LSNIF_INVALID_ARGUMENT, "null output handle");
+  int ndev = 0;
+  ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+  if (device < 0 || device >= ndev) fail(LSNIF_INVALID_ARGUMENT, "invalid device ordinal");
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop{};
+  ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10)
+    fail(LSNIF_UNSUPPORTED, std::string("liblsnif_gpu is built for sm_100a; device is ") + prop.name);
+  auto M = std::make_unique<lsnif_model_s>();
+  M->device = device;
+  M->num_sms = prop.multiProcessorCount;
+  build_model(*M, d);
+  *out = M.release();
+}
+
+void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, lsnif_hit* d_hits,
+               cudaStream_t st) {
+  if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
+  if (mode != LSNIF_QUERY_CLOSEST && mode != LSNIF_QUERY_ANY) fail(LSNIF_INVALID_ARGUMENT, "bad query mode");
+  if (n > 0 && (!d_rays || !d_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
+  if (n > INT32_MAX) fail(LSNIF_INVALID_ARGUMENT, "more than 2^31-1 rays in one call");
+  ck(cudaSetDevice(M.device), "cudaSetDevice");
+  Workspace& w = M.workspace(st, std::max<int64_t>(n, 1));
+  ck(cudaMemsetAsync(w.stats, 0, 64, st), "cudaMemsetAsync");
+  w.last_rays = n;
+  for (int64_t s = 0; s < n; s += kChunk) {
+    const int64_t cn = std::min(kChunk, n - s);
+    ck(cudaMemsetAsync(w.counter, 0, 4, st), "cudaMemsetAsync");
+    lsnif_dev::TraceParams tp{};
+    tp.m = M.dm;
+    tp.rays = d_rays + s;
+    tp.n = cn;
+    tp.mode = mode;
+    tp.out = d_hits + s;
+    tp.X = w.X;
+    tp.meta = w.meta;
+    tp.row_counter = w.counter;
+    tp.stats = w.stats;
+    tp.tile_bytes = M.tile_bytes();
+    ck(lsnif_dev::launch_trace(tp, false, st), "trace_encode_kernel");
+    lsnif_dev::MlpParams mp{};
+    mp.m = M.dm;
+    mp.X = w.X;
+    mp.meta = w.meta;
+    mp.row_counter = w.counter;
+    mp.out = d_hits + s;
+    mp.tile_bytes = M.tile_bytes();
+    mp.mode = mode;
+    ck(lsnif_dev::launch_mlp(mp, static_cast<int>((cn + kTileM - 1) / kTileM), M.num_sms, st),
+       "mlp_tc_kernel");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lsnif_last_error(void) { return g_err.c_str(); }
+
+const char* lsnif_build_info(void) {
+  return "liblsnif_gpu sm_100a: trace_encode_kernel + mlp_tc_kernel (tcgen05 kind::f16, TMEM), "
+         "infer_f32_kernel";
+}
+
+lsnif_status lsnif_model_create(const lsnif_model_desc* desc, int device, lsnif_model* out) {
+  return guarded([&] {
+    if (!desc) fail(LSNIF_INVALID_ARGUMENT, "null model description");
+    create_into(*desc, device, out);
+  });
+}
+
+lsnif_status lsnif_model_load(const char* path, int device, lsnif_model* out) {
+  return guarded([&] {
+    if (!path) fail(LSNIF_INVALID_ARGUMENT, "null path");
+    FileModel fm;
+    read_model_file(path, fm);
+    create_into(fm.desc, device, out);
+  });
+}
+
+lsnif_status lsnif_model_destroy(lsnif_model model) {
+  return guarded([&] { delete model; });
+}
+
+lsnif_status lsnif_model_get_info(lsnif_model model, lsnif_model_info* out) {
+  return guarded([&] {
+    check_model(model);
+    if (!out) fail(LSNIF_INVALID_ARGUMENT, "null output");
+    *out = model->info;
+  });
+}
+
+lsnif_status lsnif_query(lsnif_model model, const lsnif_ray* d_rays, int64_t n, int mode,
+                         lsnif_hit* d_hits, void* stream) {
+  return guarded([&] {
+    check_model(model);
+    run_query(*model, d_rays, n, mode, d_hits, static_cast<cudaStream_t>(stream));
+  });
+}
+
+lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_t n, int mode,
+                              lsnif_hit* h_hits, void* stream) {
+  return guarded([&] {
+    check_model(model);
+    if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
+    if (n > 0 && (!h_rays || !h_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
+    ck(cudaSetDevice(model->device), "cudaSetDevice");
+    std::lock_guard<std::mutex> lock(model->staging_mu);
+    if (!model->staging) {
+      auto s = std::make_unique<HostStaging>();
+      for (int i = 0; i < 2; ++i) {
+        ck(cudaStreamCreateWithFlags(&s->streams[i], cudaStreamNonBlocking), "cudaStreamCreate");
+        ck(cudaMalloc(&s->d_rays[i], kHostChunk * sizeof(lsnif_ray)), "cudaMalloc(staging)");
+        ck(cudaMalloc(&s->d_hits[i], kHostChunk * sizeof(lsnif_hit)), "cudaMalloc(staging)");
+      }
+      s->cap = kHostChunk;
+      model->staging = std::move(s);
+    }
+    HostStaging& S = *model->staging;
+    // Order the staging streams after prior work on the caller's stream.
+    cudaEvent_t ev;
+    ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventRecord(ev, static_cast<cudaStream_t>(stream)), "cudaEventRecord");
+    for (int i = 0; i < 2; ++i) ck(cudaStreamWaitEvent(S.streams[i], ev, 0), "cudaStreamWaitEvent");
+    int64_t k = 0;
+    for (int64_t s = 0; s < n; s += S.cap, ++k) {
+      const int slot = static_cast<int>(k & 1);
+      const int64_t cn = std::min(S.cap, n - s);
+      cudaStream_t st = S.streams[slot];
+      ck(cudaMemcpyAsync(S.d_rays[slot], h_rays + s, cn * sizeof(lsnif_ray), cudaMemcpyHostToDevice, st),
+         "cudaMemcpyAsync(H2D)");
+      run_query(*model, S.d_rays[slot], cn, mode, S.d_hits[slot], st);
+      ck(cudaMemcpyAsync(h_hits + s, S.d_hits[slot], cn * sizeof(lsnif_hit), cudaMemcpyDeviceToHost, st),
+         "cudaMemcpyAsync(D2H)");
+    }
+    for (int i = 0; i < 2; ++i) ck(cudaStreamSynchronize(S.streams[i]), "cudaStreamSynchronize");
+    cudaEventDestroy(ev);
+  });
+}
+
+lsnif_status lsnif_infer_batch(lsnif_model model, const float* d_inputs, int64_t rows, int64_t n,
+                               const lsnif_interval* d_intervals, int64_t n_intervals,
+                               lsnif_hit* d_hits, void* stream) {
+  return guarded([&] {
+    check_model(model);
+    if (n != n_intervals) fail(LSNIF_INVALID_ARGUMENT, "infer_batch: inputs/intervals size mismatch");
+    if (rows != model->dm.K1) fail(LSNIF_INVALID_ARGUMENT, "infer_batch: input width mismatch");
+    if (n > 0 && (!d_inputs || !d_intervals || !d_hits)) fail(LSNIF_INVALID_ARGUMENT, "null pointer");
+    ck(cudaSetDevice(model->device), "cudaSetDevice");
+    ck(lsnif_dev::launch_infer_f32(model->dm, d_inputs, n, d_intervals, d_hits,
+                                   static_cast<cudaStream_t>(stream)),
+       "infer_f32_kernel");
+  });
+}
+
+lsnif_status lsnif_debug_traverse(lsnif_model model, const lsnif_ray* d_rays, int64_t n, int32_t* info,
+                                  float* interval, float* t, float* pts, uint32_t* cells, uint32_t* hidx,
+                                  float* feat, void* stream) {
+  return guarded([&] {
+    check_model(model);
+    if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
+    if (n == 0) return;
+    if (!d_rays || !info || !interval || !t || !pts || !cells || !hidx || !feat)
+      fail(LSNIF_INVALID_ARGUMENT, "null pointer");
+    ck(cudaSetDevice(model->device), "cudaSetDevice");
+    const DevModel& m = model->dm;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t H = m.H, L = m.L;
+    ck(cudaMemsetAsync(t, 0, n * H * 4, st), "memset");
+    ck(cudaMemsetAsync(pts, 0, n * H * 12, st), "memset");
+    ck(cudaMemsetAsync(cells, 0xff, n * H * 4, st), "memset");
+    ck(cudaMemsetAsync(hidx, 0xff, n * H * L * 8 * 4, st), "memset");
+    ck(cudaMemsetAsync(feat, 0, n * static_cast<size_t>(m.K1) * 4, st), "memset");
+    lsnif_dev::TraceParams tp{};
+    tp.m = m;
+    tp.rays = d_rays;
+    tp.n = n;
+    tp.info = info;
+    tp.interval = interval;
+    tp.t = t;
+    tp.pts = pts;
+    tp.cells = cells;
+    tp.hidx = hidx;
+    tp.feat = feat;
+    ck(lsnif_dev::launch_trace(tp, true, st), "trace_encode_kernel<debug>");
+  });
+}
+
+lsnif_status lsnif_last_query_stats(lsnif_model model, void* stream, lsnif_query_stats* out) {
+  return guarded([&] {
+    check_model(model);
+    if (!out) fail(LSNIF_INVALID_ARGUMENT, "null output");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Workspace* w = nullptr;
+    {
+      std::lock_guard<std::mutex> lock(model->mu);
+      auto it = model->ws.find(st);
+      if (it == model->ws.end()) fail(LSNIF_INVALID_ARGUMENT, "no query has run on this stream");
+      w = it->second.get();
+    }
+    ck(cudaSetDevice(model->device), "cudaSetDevice");
+    unsigned long long s[4];
+    ck(cudaMemcpyAsync(s, w->stats, sizeof(s), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    out->rays = w->last_rays;
+    out->pairs = static_cast<int64_t>(s[0]);
+    out->mlp_rows = static_cast<int64_t>(s[1]);
+    out->points = static_cast<int64_t>(s[2]);
+    out->volume_points = static_cast<int64_t>(s[3]);
+  });
+}
+
+}  // extern "C"

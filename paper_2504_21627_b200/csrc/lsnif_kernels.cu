@@ -1,0 +1,455 @@
+// LSNIF query kernels for sm_100a.
+//
+//  trace_encode_kernel<DEBUG>  one thread per ray: frame-box pair test,
+//      3D-DDA over the SMEM-resident occupancy bitset (points pooled per
+//      warp in SMEM), then a warp-cooperative encode of the pooled points
+//      (full SIMT efficiency regardless of per-ray point counts). Rays with
+//      >= 1 point get a compacted row of the fp16 MLP operand X, written in
+//      the UMMA canonical tile layout; other rays are answered directly.
+//      DEBUG=true writes the bit-exactness probe instead of X.
+//  mlp_tc_kernel   per 128-row tile: bulk-copy X into SMEM, three
+//      tcgen05.mma layers (fp16 x fp16 -> fp32 in TMEM, biases folded in as
+//      a constant operand column), leaky-ReLU epilogues TMEM -> regs -> SMEM,
+//      head decode + accept rule in the last epilogue, results scattered to
+//      the caller's hit array.
+//  infer_f32_kernel  fp32 CUDA-core infer_batch (renderer.cpp:183-226).
+#include <cuda_runtime.h>
+
+#include "lsnif_device.cuh"
+#include "lsnif_internal.hpp"
+#include "tc_ptx.cuh"
+
+namespace lsnif_dev {
+
+// ======================================================= trace + encode
+
+template <bool DEBUG>
+__global__ void __launch_bounds__(128) trace_encode_kernel(const TraceParams P) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const DevModel& m = P.m;
+  const int occ_words = (m.V * m.V * m.V) >> 5;
+  for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.occ + i);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  float4* pool = reinterpret_cast<float4*>(smem + ((occ_words + 3) & ~3)) + warp * (m.H * 32);
+  __syncthreads();
+
+  const int64_t ray_idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool live = ray_idx < P.n;
+  float o[3] = {0, 0, 0}, d[3] = {0, 0, 0}, t_min = 0.0f, t_max = 0.0f;
+  if (live) {
+    const float4* r4 = reinterpret_cast<const float4*>(P.rays + ray_idx);
+    const float4 a = __ldg(r4), b = __ldg(r4 + 1);
+    o[0] = a.x; o[1] = a.y; o[2] = a.z;
+    d[0] = a.w; d[1] = b.x; d[2] = b.y;
+    t_min = b.z; t_max = b.w;
+  }
+  float enter = 0.0f, exit = 0.0f;
+  const bool pair = live && frame_interval(m, o, d, t_min, t_max, enter, exit);
+
+  // ---- DDA: occupied-cell entry points into this lane's pool column
+  int count = 0;
+  bool fio = false;
+  if (pair) {
+    DdaState s;
+    if (dda_setup(m, o, d, t_min, s)) {
+      while (true) {
+        if (occ_test(smem, m.V, s.cell[0], s.cell[1], s.cell[2])) {
+          float p[3];
+          dda_entry_point(s, m.inv_fres, p);
+          if (s.entry_axis < 0 && count == 0) fio = true;
+          pool[count * 32 + lane] = make_float4(p[0], p[1], p[2], s.entry_t);
+          if (DEBUG)
+            P.cells[ray_idx * m.H + count] = static_cast<uint32_t>(s.cell[0]) |
+                                             static_cast<uint32_t>(s.cell[1]) << 8 |
+                                             static_cast<uint32_t>(s.cell[2]) << 16;
+          ++count;
+          if (count >= m.H) break;
+        }
+        if (!dda_advance(s, m.V)) break;
+      }
+    }
+  }
+
+  // ---- rays answered without the MLP
+  if (!DEBUG) {
+    if (live && !pair) {
+      lsnif_hit h{};
+      store_hit(P.out + ray_idx, h);
+    } else if (pair && count == 0) {
+      lsnif_hit h;
+      decode_hit(m.z_zero, m.n_mat, enter, exit, t_min, t_max, P.mode, true, h);
+      store_hit(P.out + ray_idx, h);
+    }
+  } else if (live) {
+    P.info[ray_idx] = pair ? (count | (fio ? 1 << 8 : 0) | (1 << 9)) : 0;
+    P.interval[2 * ray_idx] = pair ? enter : 0.0f;
+    P.interval[2 * ray_idx + 1] = pair ? exit : 0.0f;
+  }
+
+  // ---- row allocation (warp-aggregated) for rays that need the MLP
+  const bool valid = pair && count > 0;
+  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  int row = 0;
+  if (!DEBUG) {
+    int base = 0;
+    if (lane == 0 && vmask) base = atomicAdd(P.row_counter, __popc(vmask));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    row = base + __popc(vmask & lt_mask);
+    if (valid) {
+      RowMeta rm;
+      rm.ray = static_cast<int32_t>(ray_idx);
+      rm.enter = enter;
+      rm.exit = exit;
+      rm.t_min = t_min;
+      rm.t_max = t_max;
+      rm.pad[0] = rm.pad[1] = rm.pad[2] = 0;
+      float4* dst = reinterpret_cast<float4*>(P.meta + row);
+      dst[0] = make_float4(__int_as_float(rm.ray), rm.enter, rm.exit, rm.t_min);
+      dst[1] = make_float4(rm.t_max, 0.0f, 0.0f, 0.0f);
+    }
+    // query statistics (pairs, MLP rows, points, volume points)
+    const int n_pair = __popc(__ballot_sync(0xffffffffu, pair));
+    const int n_pts = __reduce_add_sync(0xffffffffu, valid ? count : 0);
+    const int n_vol = __popc(__ballot_sync(0xffffffffu, valid && fio));
+    if (lane == 0 && n_pair) {
+      atomicAdd(P.stats + 0, static_cast<unsigned long long>(n_pair));
+      atomicAdd(P.stats + 1, static_cast<unsigned long long>(__popc(vmask)));
+      atomicAdd(P.stats + 2, static_cast<unsigned long long>(n_pts));
+      atomicAdd(P.stats + 3, static_cast<unsigned long long>(n_vol));
+    }
+  }
+
+  // ---- warp-cooperative encode of all pooled points
+  const int c = valid ? count : 0;
+  int incl = c;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += v;
+  }
+  const int excl = incl - c;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  const unsigned fio_mask = __ballot_sync(0xffffffffu, valid && fio);
+  const float scale = m.act_scale;
+  const int LF = m.LF, F = m.F;
+  for (int jb = 0; jb < total; jb += 32) {
+    const int j = jb + lane;
+    int owner = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+      const int ex = __shfl_sync(0xffffffffu, excl, owner + step);
+      if (ex <= j) owner += step;
+    }
+    const int o_excl = __shfl_sync(0xffffffffu, excl, owner);
+    const int o_row = __shfl_sync(0xffffffffu, row, owner);
+    const long long o_ray = __shfl_sync(0xffffffffu, static_cast<long long>(ray_idx), owner);
+    if (j >= total) continue;
+    const int k = j - o_excl;
+    const float4 pp = pool[k * 32 + owner];
+    const float p[3] = {pp.x, pp.y, pp.z};
+    const bool volume = (k == 0) && ((fio_mask >> owner) & 1u);
+    float fv[16];
+    for (int l = 0; l < m.L; ++l) {
+      float feat[4];
+      uint32_t hidx[8];
+      encode_point_level(m, l, p, volume, feat, DEBUG ? hidx : nullptr);
+      if (DEBUG) {
+        const int64_t hb = ((o_ray * m.H + k) * m.L + l) * 8;
+        const int nc = volume ? 8 : 4;
+        for (int q = 0; q < nc; ++q) P.hidx[hb + q] = hidx[q];
+        for (int f = 0; f < F; ++f) P.feat[o_ray * m.K1 + k * LF + l * F + f] = feat[f];
+      }
+#pragma unroll
+      for (int f = 0; f < 4; ++f)
+        if (f < F) fv[l * F + f] = feat[f];
+    }
+    if (DEBUG) {
+      P.t[o_ray * m.H + k] = pp.w;
+      P.pts[(o_ray * m.H + k) * 3 + 0] = pp.x;
+      P.pts[(o_ray * m.H + k) * 3 + 1] = pp.y;
+      P.pts[(o_ray * m.H + k) * 3 + 2] = pp.z;
+    } else {
+      uint8_t* tile = P.X + static_cast<int64_t>(o_row >> 7) * P.tile_bytes;
+      const int r = o_row & 127;
+      const int col0 = k * LF;
+      if ((LF & 1) == 0) {
+        for (int q = 0; q < LF; q += 2) {
+          const __half2 hv = __floats2half2_rn(__fmul_rn(fv[q], scale), __fmul_rn(fv[q + 1], scale));
+          *reinterpret_cast<__half2*>(tile + canon_offset(r, col0 + q, kTileM)) = hv;
+        }
+      } else {
+        for (int q = 0; q < LF; ++q)
+          *reinterpret_cast<__half*>(tile + canon_offset(r, col0 + q, kTileM)) =
+              __float2half_rn(__fmul_rn(fv[q], scale));
+      }
+    }
+  }
+
+  // ---- zero padding of the row tail + bias constant column (encoding.hpp:170)
+  if (!DEBUG && valid) {
+    uint8_t* tile = P.X + static_cast<int64_t>(row >> 7) * P.tile_bytes;
+    const int r = row & 127;
+    const __half hs = __float2half_rn(scale);
+    const __half hz = __float2half_rn(0.0f);
+    int col = count * LF;
+    for (; col < m.K1P && (col & 7); ++col)
+      *reinterpret_cast<__half*>(tile + canon_offset(r, col, kTileM)) = (col == m.K1) ? hs : hz;
+    for (; col < m.K1P; col += 8) {
+      __align__(16) __half v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = (col + q == m.K1) ? hs : hz;
+      *reinterpret_cast<uint4*>(tile + canon_offset(r, col, kTileM)) =
+          *reinterpret_cast<const uint4*>(v);
+    }
+  }
+}
+
+// ============================================================ tcgen05 MLP
+
+// Shared-memory plan (bytes, all 1024-aligned): W1 | W2 | W3 | XH | bars.
+template <int HID>
+struct MlpSmem {
+  static constexpr int kK2 = HID + 16;                 // hidden + bias block
+  static constexpr int kXHBytes = kTileM * kK2 * 2;    // holds X (K1P <= K2) or H
+};
+
+template <int HID>
+__global__ void __launch_bounds__(128, 1) mlp_tc_kernel(const MlpParams P) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const DevModel& m = P.m;
+  constexpr int K2 = MlpSmem<HID>::kK2;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW1 = base;
+  uint8_t* sW2 = sW1 + m.w1_bytes;
+  uint8_t* sW3 = sW2 + m.w2_bytes;
+  uint8_t* sXH = sW3 + ((m.w3_bytes + 1023) & ~1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sXH + MlpSmem<HID>::kXHBytes);
+  uint64_t* bar_load = bars;
+  uint64_t* bar_mma = bars + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+
+  const int rows = *P.row_counter;
+  const int ntiles = (rows + kTileM - 1) / kTileM;
+  if (static_cast<int>(blockIdx.x) >= ntiles) return;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  if (tid == 0) {
+    tc::mbar_init(bar_load, 1);
+    tc::mbar_init(bar_mma, 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, HID);  // D reused by the three layers
+  // Bias block of the hidden operand: column HID = act_scale, HID+1..K2-1 = 0.
+  {
+    const __half hs = __float2half_rn(m.act_scale);
+    const __half hz = __float2half_rn(0.0f);
+    __align__(16) __half v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = q == 0 ? hs : hz;
+    *reinterpret_cast<uint4*>(sXH + canon_offset(tid, HID, kTileM)) = *reinterpret_cast<const uint4*>(v);
+    *reinterpret_cast<uint4*>(sXH + canon_offset(tid, HID + 8, kTileM)) = make_uint4(0, 0, 0, 0);
+  }
+  tc::fence_proxy_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (tid == 0) {
+    tc::mbar_arrive_expect_tx(bar_load, m.w1_bytes + m.w2_bytes + m.w3_bytes);
+    tc::bulk_g2s(sW1, m.w_canon, m.w1_bytes, bar_load);
+    tc::bulk_g2s(sW2, m.w_canon + m.w1_bytes, m.w2_bytes, bar_load);
+    tc::bulk_g2s(sW3, m.w_canon + m.w1_bytes + m.w2_bytes, m.w3_bytes, bar_load);
+  }
+  uint32_t load_phase = 0, mma_phase = 0;
+  tc::mbar_wait(bar_load, load_phase);
+  load_phase ^= 1;
+
+  const uint32_t x_bytes = static_cast<uint32_t>(kTileM) * m.K1P * 2;
+  const uint32_t sXH_a = tc::smem_addr(sXH);
+  const uint32_t sW1_a = tc::smem_addr(sW1), sW2_a = tc::smem_addr(sW2), sW3_a = tc::smem_addr(sW3);
+  constexpr uint32_t kIdescH = tc::idesc_f16_f32(kTileM, HID);
+  const uint32_t idesc3 = tc::idesc_f16_f32(kTileM, m.N3);
+  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+  const uint32_t a_lbo = kTileM * 16;  // K-chunk stride of the 128-row A operand
+
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // ---- X tile -> SMEM
+    if (tid == 0) {
+      tc::mbar_arrive_expect_tx(bar_load, x_bytes);
+      tc::bulk_g2s(sXH, P.X + static_cast<int64_t>(tile) * P.tile_bytes, x_bytes, bar_load);
+    }
+    tc::mbar_wait(bar_load, load_phase);
+    load_phase ^= 1;
+
+    // ---- three layers; hidden epilogues write back into sXH
+#pragma unroll 1
+    for (int layer = 0; layer < 3; ++layer) {
+      if (tid == 0) {
+        tc::tc_fence_after();
+        const int ksteps = (layer == 0 ? m.K1P : K2) / 16;
+        const uint32_t b_base = layer == 0 ? sW1_a : layer == 1 ? sW2_a : sW3_a;
+        const uint32_t b_rows = layer == 2 ? m.N3 : HID;
+        const uint32_t idesc = layer == 2 ? idesc3 : kIdescH;
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const uint64_t ad = tc::smem_desc(sXH_a + ks * 2 * a_lbo, a_lbo, 128);
+          const uint64_t bd = tc::smem_desc(b_base + ks * 2 * b_rows * 16, b_rows * 16, 128);
+          tc::mma_f16_ss(tmem, ad, bd, idesc, ks > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(bar_mma);
+      }
+      tc::mbar_wait(bar_mma, mma_phase);
+      mma_phase ^= 1;
+      tc::tc_fence_after();
+
+      if (layer < 2) {
+        // h = leaky(acc) (bias already accumulated; the activation scale
+        // carries through the positively homogeneous leaky-ReLU)
+#pragma unroll
+        for (int cb = 0; cb < HID; cb += 32) {
+          uint32_t acc[32];
+          tc::tmem_ld32(tmem + lane_base + cb, acc);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 32; q += 8) {
+            __align__(16) __half2 hv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float v0 = __uint_as_float(acc[q + 2 * e]);
+              float v1 = __uint_as_float(acc[q + 2 * e + 1]);
+              v0 = fmaxf(v0, __fmul_rn(v0, 0.01f));
+              v1 = fmaxf(v1, __fmul_rn(v1, 0.01f));
+              hv[e] = __floats2half2_rn(v0, v1);
+            }
+            *reinterpret_cast<uint4*>(sXH + canon_offset(tid, cb + q, kTileM)) =
+                *reinterpret_cast<const uint4*>(hv);
+          }
+        }
+        tc::fence_proxy_async_smem();
+        tc::tc_fence_before();
+        __syncthreads();
+      } else {
+        // ---- heads + decode + accept (renderer.cpp:208-223, 280-301)
+        const int row = tile * kTileM + tid;
+        float z[32];
+        for (int cb = 0; cb < m.N3; cb += 16) {
+          uint32_t acc[16];
+          tc::tmem_ld16(tmem + lane_base + cb, acc);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 16; ++q) z[cb + q] = __fmul_rn(__uint_as_float(acc[q]), m.inv_act_scale);
+        }
+        if (row < rows) {
+          const float4* mp = reinterpret_cast<const float4*>(P.meta + row);
+          const float4 a = mp[0];
+          const float4 b = mp[1];
+          lsnif_hit h;
+          decode_hit(z, m.n_mat, a.y, a.z, a.w, b.x, P.mode, true, h);
+          store_hit(P.out + __float_as_int(a.x), h);
+        }
+        tc::tc_fence_before();
+        __syncthreads();
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, HID);
+  }
+}
+
+// ==================================================== fp32 infer_batch
+
+// One thread per column; exact fp32, sequential sum over the input index
+// (the oracle's order), unfused multiply-add.
+__global__ void __launch_bounds__(128) infer_f32_kernel(const DevModel m, const float* __restrict__ x,
+                                                        int64_t n, const lsnif_interval* __restrict__ iv,
+                                                        lsnif_hit* __restrict__ out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int in = m.K1, hid = m.hidden, no = m.n_out;
+  const float* w1 = m.w_f32;
+  const float* b1 = w1 + hid * in;
+  const float* w2 = b1 + hid;
+  const float* b2 = w2 + hid * hid;
+  const float* w3 = b2 + hid;
+  const float* b3 = w3 + no * hid;
+  const float* xc = x + j * in;
+  float h1[256], h2[256], z[32];
+  for (int i = 0; i < hid; ++i) {
+    float s = 0.0f;
+    for (int k = 0; k < in; ++k) s = __fadd_rn(s, __fmul_rn(w1[i * in + k], xc[k]));
+    s = __fadd_rn(s, b1[i]);
+    h1[i] = s < 0.0f ? __fmul_rn(s, 0.01f) : s;
+  }
+  for (int i = 0; i < hid; ++i) {
+    float s = 0.0f;
+    for (int k = 0; k < hid; ++k) s = __fadd_rn(s, __fmul_rn(w2[i * hid + k], h1[k]));
+    s = __fadd_rn(s, b2[i]);
+    h2[i] = s < 0.0f ? __fmul_rn(s, 0.01f) : s;
+  }
+  for (int i = 0; i < no; ++i) {
+    float s = 0.0f;
+    for (int k = 0; k < hid; ++k) s = __fadd_rn(s, __fmul_rn(w3[i * hid + k], h2[k]));
+    z[i] = __fadd_rn(s, b3[i]);
+  }
+  lsnif_hit h;
+  decode_hit(z, m.n_mat, iv[j].enter, iv[j].exit, 0.0f, 0.0f, LSNIF_QUERY_CLOSEST, false, h);
+  store_hit(out + j, h);
+}
+
+// ================================================================ launch
+
+size_t trace_smem_bytes(const DevModel& m) {
+  const size_t occ_words = (static_cast<size_t>(m.V) * m.V * m.V) >> 5;
+  return ((occ_words + 3) & ~size_t(3)) * 4 + 4 * static_cast<size_t>(m.H) * 32 * 16;
+}
+
+size_t mlp_smem_bytes(const DevModel& m) {
+  const size_t xh = static_cast<size_t>(kTileM) * (m.hidden + 16) * 2;
+  return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + xh + 64;
+}
+
+cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st) {
+  if (p.n <= 0) return cudaSuccess;
+  const size_t smem = trace_smem_bytes(p.m);
+  const unsigned blocks = static_cast<unsigned>((p.n + 127) / 128);
+  if (debug) {
+    cudaFuncSetAttribute(trace_encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    trace_encode_kernel<true><<<blocks, 128, smem, st>>>(p);
+  } else {
+    cudaFuncSetAttribute(trace_encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    trace_encode_kernel<false><<<blocks, 128, smem, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st) {
+  if (max_tiles <= 0) return cudaSuccess;
+  const size_t smem = mlp_smem_bytes(p.m);
+  const int ctas_per_sm = smem <= 113 * 1024 ? 2 : 1;
+  const unsigned grid = static_cast<unsigned>(std::min(max_tiles, num_sms * ctas_per_sm));
+  if (p.m.hidden == 128) {
+    cudaFuncSetAttribute(mlp_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    mlp_tc_kernel<128><<<grid, 128, smem, st>>>(p);
+  } else {
+    cudaFuncSetAttribute(mlp_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    mlp_tc_kernel<64><<<grid, 128, smem, st>>>(p);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_infer_f32(const DevModel& m, const float* x, int64_t n, const lsnif_interval* iv,
+                             lsnif_hit* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  infer_f32_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(m, x, n, iv, out);
+  return cudaGetLastError();
+}
+
+}  // namespace lsnif_dev

@@ -1,0 +1,220 @@
+"""Python host mirror of the reference's LSNIF query API over the C ABI
+(include/lsnif_gpu.h, liblsnif_gpu.so built in-tree for sm_100a).
+
+Reference interface mirrored (proj/include/lsnif/renderer.hpp):
+  * ``load_model(path)``                    -> model_io.hpp:45 (+ device upload)
+  * ``infer_batch(model, inputs, intervals)`` -> renderer.hpp:52-53
+  * ``GpuModel.intersect(rays)``             -> intersect_scene's narrow phase +
+                                               closest-hit accept (renderer.cpp:269-303)
+  * ``GpuModel.occluded(rays)``              -> occluded_batch (renderer.cpp:305-323)
+Errors are raised as the reference's exception types: ValueError for
+std::invalid_argument, RuntimeError for std::runtime_error.
+
+There is no CPU fallback: importing a missing/unloadable extension raises.
+PyTorch is used only for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "liblsnif_gpu.so")
+
+RAY_DTYPE = np.dtype([("o", "<f4", 3), ("d", "<f4", 3), ("t_min", "<f4"), ("t_max", "<f4")])
+HIT_DTYPE = np.dtype([("flags_material", "<u4"), ("t_world", "<f4"), ("normal", "<f4", 3),
+                      ("albedo", "<f4", 3)])
+PAIR, OCCLUDED, ACCEPTED = 1, 2, 4
+CLOSEST, ANY = 0, 1
+
+OK, INVALID_ARGUMENT, RUNTIME_ERROR, CUDA_ERROR, UNSUPPORTED = range(5)
+
+
+class LsnifError(RuntimeError):
+    pass
+
+
+class ModelInfo(C.Structure):
+    _fields_ = [("voxel_res", C.c_int32), ("hit_cap", C.c_int32), ("n_levels", C.c_int32),
+                ("f_dim", C.c_int32), ("table_size", C.c_uint32), ("hidden", C.c_int32),
+                ("n_mat", C.c_int32), ("n_materials", C.c_int32), ("level_res", C.c_int32 * 4),
+                ("aabb", C.c_float * 6), ("activation_scale", C.c_float),
+                ("device_bytes", C.c_uint64)]
+
+
+class QueryStats(C.Structure):
+    _fields_ = [("rays", C.c_int64), ("pairs", C.c_int64), ("mlp_rows", C.c_int64),
+                ("points", C.c_int64), ("volume_points", C.c_int64)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> C.CDLL:
+    """Loads liblsnif_gpu.so; raises if it is missing (no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise LsnifError(f"liblsnif_gpu.so not built at {path}; run `make` "
+                         "(or __graft_entry__.build())")
+    lib = C.CDLL(path)
+    P = C.c_void_p
+    lib.lsnif_last_error.restype = C.c_char_p
+    lib.lsnif_build_info.restype = C.c_char_p
+    lib.lsnif_model_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(P)]
+    lib.lsnif_model_destroy.argtypes = [P]
+    lib.lsnif_model_get_info.argtypes = [P, C.POINTER(ModelInfo)]
+    lib.lsnif_query.argtypes = [P, P, C.c_int64, C.c_int, P, P]
+    lib.lsnif_query_host.argtypes = [P, P, C.c_int64, C.c_int, P, P]
+    lib.lsnif_infer_batch.argtypes = [P, P, C.c_int64, C.c_int64, P, C.c_int64, P, P]
+    lib.lsnif_debug_traverse.argtypes = [P, P, C.c_int64] + [P] * 7 + [P]
+    lib.lsnif_last_query_stats.argtypes = [P, P, C.POINTER(QueryStats)]
+    for name in ("lsnif_model_load", "lsnif_model_destroy", "lsnif_model_get_info", "lsnif_query",
+                 "lsnif_query_host", "lsnif_infer_batch", "lsnif_debug_traverse",
+                 "lsnif_last_query_stats"):
+        getattr(lib, name).restype = C.c_int
+    _lib = lib
+    return lib
+
+
+def _check(st: int) -> None:
+    if st == OK:
+        return
+    msg = load_library().lsnif_last_error().decode()
+    if st == INVALID_ARGUMENT:
+        raise ValueError(msg)
+    raise LsnifError(f"lsnif status {st}: {msg}")
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class GpuModel:
+    """A device-resident LSNIF model (one per object; shareable across instances)."""
+
+    def __init__(self, path: str, device: int = 0):
+        lib = load_library()
+        h = C.c_void_p()
+        _check(lib.lsnif_model_load(path.encode(), device, C.byref(h)))
+        self.h = h
+        self.device = device
+        info = ModelInfo()
+        _check(lib.lsnif_model_get_info(self.h, C.byref(info)))
+        self.info = info
+        self.H, self.n_levels, self.F = info.hit_cap, info.n_levels, info.f_dim
+        self.input_width = self.H * self.n_levels * self.F
+        self.aabb = np.array(list(info.aabb), np.float32)
+
+    def close(self):
+        if getattr(self, "h", None):
+            load_library().lsnif_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- device API (torch CUDA tensors) ----
+    def query(self, rays, mode: int = CLOSEST, out=None, stream=None):
+        """rays: CUDA tensor (n, 8) float32 (lsnif_ray records). Returns (n, 8)
+        int32 tensor of lsnif_hit records (view with hits_to_numpy)."""
+        torch = _torch()
+        assert rays.is_cuda and rays.dtype == torch.float32 and rays.shape[-1] == 8
+        rays = rays.contiguous()
+        n = rays.shape[0]
+        if out is None:
+            out = torch.empty((n, 8), dtype=torch.int32, device=rays.device)
+        _check(load_library().lsnif_query(self.h, rays.data_ptr(), n, mode, out.data_ptr(),
+                                          _stream_ptr(stream)))
+        return out
+
+    def last_stats(self, stream=None) -> dict:
+        s = QueryStats()
+        _check(load_library().lsnif_last_query_stats(self.h, _stream_ptr(stream), C.byref(s)))
+        return {k: int(getattr(s, k)) for k, _ in QueryStats._fields_}
+
+    def debug_traverse(self, rays) -> dict:
+        torch = _torch()
+        rays = rays.contiguous()
+        n, H, L, F = rays.shape[0], self.H, self.n_levels, self.F
+        dev = rays.device
+        out = dict(info=torch.empty(n, dtype=torch.int32, device=dev),
+                   interval=torch.empty((n, 2), dtype=torch.float32, device=dev),
+                   t=torch.empty((n, H), dtype=torch.float32, device=dev),
+                   pts=torch.empty((n, H, 3), dtype=torch.float32, device=dev),
+                   cells=torch.empty((n, H), dtype=torch.int32, device=dev),
+                   hidx=torch.empty((n, H, L, 8), dtype=torch.int32, device=dev),
+                   feat=torch.empty((n, H * L * F), dtype=torch.float32, device=dev))
+        _check(load_library().lsnif_debug_traverse(
+            self.h, rays.data_ptr(), n, *[out[k].data_ptr() for k in
+                                          ("info", "interval", "t", "pts", "cells", "hidx", "feat")],
+            _stream_ptr(None)))
+        return out
+
+    def infer_batch(self, inputs, intervals, stream=None):
+        """infer_batch (renderer.cpp:183-226). inputs: CUDA (n, input_width)
+        fp32 — row j is column j of the reference's MatX; intervals (n, 2)."""
+        torch = _torch()
+        inputs = inputs.contiguous()
+        intervals = intervals.contiguous()
+        n = inputs.shape[0]
+        rows = inputs.shape[1] if inputs.dim() == 2 else 0
+        out = torch.empty((n, 8), dtype=torch.int32, device=inputs.device)
+        _check(load_library().lsnif_infer_batch(self.h, inputs.data_ptr(), rows, n,
+                                                intervals.data_ptr(), intervals.shape[0],
+                                                out.data_ptr(), _stream_ptr(stream)))
+        return out
+
+    # ---- host API (numpy, the reference's by-value vectors) ----
+    def query_host(self, rays: np.ndarray, mode: int = CLOSEST, out: np.ndarray | None = None):
+        rays = np.ascontiguousarray(rays)
+        if rays.dtype != RAY_DTYPE:
+            rays = rays.astype(np.float32, copy=False).reshape(-1, 8)
+        n = len(rays)
+        if out is None:
+            out = np.empty(n, HIT_DTYPE)
+        _check(load_library().lsnif_query_host(self.h, rays.ctypes.data, n, mode, out.ctypes.data,
+                                               None))
+        return out
+
+    def intersect(self, rays: np.ndarray) -> np.ndarray:
+        """Closest-hit narrow phase for one object (intersect_scene semantics)."""
+        return self.query_host(rays, CLOSEST)
+
+    def occluded(self, rays: np.ndarray) -> np.ndarray:
+        """occluded_batch semantics: 1 where a neural hit lies in [t_min, t_max]."""
+        h = self.query_host(rays, ANY)
+        return ((h["flags_material"] & ACCEPTED) != 0).astype(np.int8)
+
+
+def load_model(path: str, device: int = 0) -> GpuModel:
+    return GpuModel(path, device)
+
+
+def infer_batch(model: GpuModel, inputs, intervals):
+    return model.infer_batch(inputs, intervals)
+
+
+def hits_to_numpy(hits) -> np.ndarray:
+    """(n, 8) int32 CUDA/CPU tensor of lsnif_hit -> numpy HIT_DTYPE records."""
+    a = hits.detach().cpu().numpy() if hasattr(hits, "detach") else np.asarray(hits)
+    return np.ascontiguousarray(a).view(HIT_DTYPE).reshape(-1)
+
+
+def rays_to_tensor(rays: np.ndarray, device="cuda"):
+    torch = _torch()
+    return torch.from_numpy(np.ascontiguousarray(rays).view(np.float32).reshape(-1, 8).copy()).to(device)
