@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""LSNIF batched ray-query benchmark on B200.
+
+Metric (BASELINE.json): LSNIF ray queries/sec, one query = one input ray
+answered (including rays that miss the frame box).
+
+Default workload (configs[1], "C2"): the teapot LSNIF fixture
+(tests/golden/teapot_seed0.lsnif: reference train() setup state, seed 0),
+1920x1080 pixel-centre camera rays answered with the closest-hit rule, plus
+one NEE shadow ray per accepted primary hit answered with the any-hit rule.
+A step = the primary query + the shadow query. Under torchrun each rank
+answers its own frame (per-GPU work fixed: weak scaling, no data-path
+collective); the timed region is max-reduced over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c1]
+  python bench.py --impl reference   # the reference's CPU algorithm (oracle port)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MODEL_PATH = os.path.join(ROOT, "tests", "golden", "teapot_seed0.lsnif")
+METRIC = "LSNIF ray queries/sec at 1/2/4/8 B200, % of roofline, vs CPU ref (cores)"
+UNIT = "rays/s"
+L2_FLUSH_BYTES = 256 << 20
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+WORKLOADS = {
+    "c2": "C2 (configs[1]): teapot LSNIF (seed-0 reference init), 1920x1080 pixel-centre "
+          "primary rays (closest-hit) + NEE shadow rays toward a point light from the "
+          "accepted primary hits (any-hit), one frame per GPU",
+    "c3": "C3 (configs[2]): teapot LSNIF, 16,777,216 incoherent rays (origins uniform in "
+          "the frame box, directions uniform on S^2, seed 3), closest-hit, per GPU",
+    "c1": "C1 (configs[0]): teapot LSNIF, 256x256 pixel-centre primary rays, closest-hit",
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=list(WORKLOADS), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=6.0,
+                    help="target CPU work per timed baseline pass")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- workload
+
+def build_rays(workload: str, rank: int, box: np.ndarray):
+    """Returns [(rays, mode)] for one rank, before shadow generation."""
+    from paper_2504_21627_b200 import workloads as W
+    if workload == "c2":
+        return W.camera_rays(1920, 1080, jitter=W.rank_jitter(rank))
+    if workload == "c1":
+        return W.camera_rays(256, 256, jitter=W.rank_jitter(rank))
+    return W.incoherent_rays(1 << 24, box, seed=3, start=rank << 24)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        d["source"] = "measured"
+        return d
+    except Exception:
+        return dict(FALLBACK_PEAKS)
+
+
+def load_traffic(workload: str):
+    p = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """Samples SM clock and clock-event reasons with NVML while running."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device: int, period_s: float = 0.005):
+        self.samples, self.reasons = [], 0
+        self.ok = False
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(get_r(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ CPU baseline
+
+def cpu_oracle(fast: bool = True):
+    from oracle import oracle as O
+    if fast:
+        O.build(fast=True)
+    return O
+
+
+def cpu_sample(primary: np.ndarray, shadow: np.ndarray, frac: float):
+    """Strided subsample of both ray sets (keeps the image-space mix)."""
+    step = max(1, int(round(1.0 / max(frac, 1e-9))))
+    return primary[::step], shadow[::step], step
+
+
+def time_cpu(O, model, primary, shadow, target_s: float):
+    """Times the oracle narrow phase (all host threads) on a sample of the
+    same workload sized for ~target_s of CPU work. Returns rays/s and info."""
+    total = len(primary) + len(shadow)
+    p0, s0, _ = cpu_sample(primary, shadow, 8192.0 / total)
+    t0 = time.perf_counter()
+    model.narrow_phase(p0, 0, 0)
+    if len(s0):
+        model.narrow_phase(s0, 1, 0)
+    est = (len(p0) + len(s0)) / max(time.perf_counter() - t0, 1e-6)
+    frac = min(1.0, target_s * est / total)
+    p1, s1, step = cpu_sample(primary, shadow, frac)
+    tp = model.time_narrow_phase(p1, 0, 0, 1)
+    ts = model.time_narrow_phase(s1, 1, 0, 1) if len(s1) else 0.0
+    n = len(p1) + len(s1)
+    return n / (tp + ts), {"rays": n, "stride": step, "seconds": tp + ts}
+
+
+# ---------------------------------------------------------------- reference
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU algorithm (oracle port of
+    run_narrow_phase + infer_batch, -O3 -march=native, all host threads) on a
+    bounded sample of this arm's workload."""
+    if rank != 0:
+        return 0
+    O = cpu_oracle(True)
+    from paper_2504_21627_b200 import workloads as W
+    model = O.OracleModel.load(MODEL_PATH, fast=True)
+    primary = build_rays(args.workload, 0, model.aabb)
+    mode0 = 0
+    cores = int(O.lib(True).oracle_hardware_concurrency())
+    # bounded sample sized for ~2 s of CPU work per step
+    probe = primary[:: max(1, len(primary) // 8192)]
+    t0 = time.perf_counter()
+    model.narrow_phase(probe, mode0, 0)
+    rate = len(probe) / max(time.perf_counter() - t0, 1e-6)
+    stride = max(1, int(len(primary) / max(rate * 2.0, 1.0)))
+    prim = primary[::stride]
+    hits = model.narrow_phase(prim, mode0, 0)
+    shadow = W.shadow_rays(prim, hits, model.aabb)[0] if args.workload == "c2" else prim[:0]
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        model.narrow_phase(prim, mode0, 0)
+        if len(shadow):
+            model.narrow_phase(shadow, 1, 0)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    n = len(prim) + len(shadow)
+    total = sum(times)
+    value = n * len(times) / total
+    sample = (f"every {stride}th ray of the {args.workload.upper()} primary set "
+              f"({len(prim)} rays) + {len(shadow)} shadow rays from the oracle's own hits")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload], "rays_per_step": n,
+                   "parallelism": "host threads (parallel_slices)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference cannot be built here (Eigen3/CLI11 absent); timed arm is the oracle's "
+                "C++ restatement of run_narrow_phase + infer_batch built with the reference's "
+                "flags (-O3 -march=native)",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------- ours
+
+def main():
+    args = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2504_21627_b200 import lsnif, workloads as W
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    model = lsnif.GpuModel(MODEL_PATH, local_rank)
+    box = model.aabb
+    primary = build_rays(args.workload, rank, box)
+    d_primary = lsnif.rays_to_tensor(primary, dev)
+    d_hits_p = torch.empty((len(primary), 8), dtype=torch.int32, device=dev)
+    mode_p = lsnif.CLOSEST
+    model.query(d_primary, mode_p, out=d_hits_p)
+    stats_p = model.last_stats()
+    hits_p = lsnif.hits_to_numpy(d_hits_p)
+    if args.workload == "c2":
+        shadow, _ = W.shadow_rays(primary, hits_p, box)
+    else:
+        shadow = primary[:0]
+    d_shadow = lsnif.rays_to_tensor(shadow, dev) if len(shadow) else None
+    d_hits_s = torch.empty((max(len(shadow), 1), 8), dtype=torch.int32, device=dev)
+    stats_s = {"rays": 0, "pairs": 0, "mlp_rows": 0, "points": 0, "volume_points": 0}
+    if len(shadow):
+        model.query(d_shadow, lsnif.ANY, out=d_hits_s)
+        stats_s = model.last_stats()
+    n_step = len(primary) + len(shadow)
+
+    def step():
+        model.query(d_primary, mode_p, out=d_hits_p)
+        if d_shadow is not None:
+            model.query(d_shadow, lsnif.ANY, out=d_hits_s)
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local_rank)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    model.profile_read(reset=True)
+    model.profile_enable(True)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()                       # L2 flush, outside the timed events
+        ev[k][0].record()
+        step()
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks.stop()
+    model.profile_enable(False)
+    prof = model.profile_read(reset=True)
+    elapsed_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    value = world * n_step * args.steps / (elapsed_ms / 1e3)
+
+    # ---- e2e: same step through the host C-ABI entry (pinned buffers)
+    pin_p = torch.from_numpy(primary.view(np.float32).reshape(-1, 8).copy()).pin_memory()
+    hp = torch.empty((len(primary), 8), dtype=torch.int32).pin_memory()
+    pin_s = torch.from_numpy(shadow.view(np.float32).reshape(-1, 8).copy()).pin_memory() \
+        if len(shadow) else None
+    hs = torch.empty((max(len(shadow), 1), 8), dtype=torch.int32).pin_memory()
+    lib = lsnif.load_library()
+
+    def e2e_step():
+        lsnif._check(lib.lsnif_query_host(model.h, pin_p.data_ptr(), len(primary), mode_p,
+                                          hp.data_ptr(), None))
+        if pin_s is not None:
+            lsnif._check(lib.lsnif_query_host(model.h, pin_s.data_ptr(), len(shadow), lsnif.ANY,
+                                              hs.data_ptr(), None))
+
+    e2e_step()
+    e2e_steps = max(3, min(args.steps, 10))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * n_step * e2e_steps / e2e_s
+    assert np.array_equal(hp.numpy(), d_hits_p.cpu().numpy()), "host/device results differ"
+
+    if rank == 0:
+        peaks = load_peaks()
+        tr_ms = prof["trace_ms"] / args.steps
+        ml_ms = prof["mlp_ms"] / args.steps
+        rows = stats_p["mlp_rows"] + stats_s["mlp_rows"]
+        pts = stats_p["points"] + stats_s["points"]
+        vol = stats_p["volume_points"] + stats_s["volume_points"]
+        # algorithmic bytes of trace_encode_kernel per step (SURVEY §8(d) B_ray,
+        # minus the 32 B results the MLP kernel writes for MLP rows)
+        trace_bytes = 32 * n_step + 32 * (n_step - rows) + 48 * pts + 48 * vol
+        mlp_flops = 2 * rows * (model.input_width * model.info.hidden + model.info.hidden ** 2 +
+                                model.info.hidden * (8 + model.info.n_mat))
+        traffic = load_traffic(args.workload)
+        if tr_ms >= ml_ms:
+            launches = max(1, prof["trace_launches"] // args.steps)
+            ach = trace_bytes / (tr_ms / 1e3) / 1e9
+            roof = {"kernel": "trace_encode_kernel", "bound": "hbm", "achieved": ach,
+                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
+                    "traffic": traffic.get("trace_encode_kernel"),
+                    "algorithmic_bytes_per_launch": trace_bytes / launches,
+                    "peak_source": peaks["source"]}
+        else:
+            launches = max(1, prof["mlp_launches"] // args.steps)
+            ach = mlp_flops / (ml_ms / 1e3) / 1e12
+            pk = peaks.get("bf16_tflops_sustained", 1400.0)
+            roof = {"kernel": "mlp_tc_kernel", "bound": "tensor", "achieved": ach, "peak": pk,
+                    "unit": "TFLOP/s", "frac": ach / pk, "traffic": traffic.get("mlp_tc_kernel"),
+                    "peak_source": peaks["source"]}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 traversal/encode + f16xf16->f32 tcgen05 MLP", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.workload], "rays_per_step_per_gpu": n_step,
+                       "primary_rays": len(primary), "shadow_rays": len(shadow),
+                       "l2": "flushed between timed steps (256 MiB write outside the events)",
+                       "parallelism": f"dp{world} (one frame per GPU, no data-path collective)"},
+            "workload_stats": {
+                "frac_hit_aabb": (stats_p["pairs"] + stats_s["pairs"]) / n_step,
+                "frac_ge1_point": rows / n_step, "mean_points": pts / n_step,
+                "volume_points": vol},
+            "roofline": roof,
+            "kernels": {"trace_encode_kernel": {"ms_per_step": tr_ms,
+                                                "launches": prof["trace_launches"]},
+                        "mlp_tc_kernel": {"ms_per_step": ml_ms,
+                                          "launches": prof["mlp_launches"],
+                                          "tflops": mlp_flops / (ml_ms / 1e3) / 1e12
+                                          if ml_ms > 0 else None}},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 32 * n_step,
+                    "d2h_bytes_per_step": 32 * n_step, "steps": e2e_steps,
+                    "api": "lsnif_query_host (pinned host rays/hits, chunked H2D/query/D2H)"},
+            "gpu_launches": prof["launches"],
+            "clocks": clocks.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                O = cpu_oracle(True)
+                om = O.OracleModel.load(MODEL_PATH, fast=True)
+                rate, info = time_cpu(O, om, primary, shadow, args.cpu_seconds)
+                cores = int(O.lib(True).oracle_hardware_concurrency())
+                line["cpu_baseline"] = {
+                    "value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                    "sample": f"every {info['stride']}th primary and shadow ray of this "
+                              f"workload ({info['rays']} rays, {info['seconds']:.1f} s)"}
+            except Exception as e:  # reported, never silently substituted
+                line["cpu_baseline"] = {"value": None, "error": str(e)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

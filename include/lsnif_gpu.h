@@ -166,6 +166,19 @@ lsnif_status lsnif_debug_traverse(lsnif_model model, const lsnif_ray* d_rays, in
 /* Counters of the most recent lsnif_query on `stream` (synchronises it). */
 lsnif_status lsnif_last_query_stats(lsnif_model model, void* stream, lsnif_query_stats* out);
 
+/* Kernel-level timing of queries (bench / roofline support). When enabled,
+ * CUDA events are recorded on the query stream around every kernel launch;
+ * lsnif_profile_read synchronises `stream` and returns the summed device
+ * durations since the last reset. `launches` counts every kernel the query
+ * entry points launched (always tracked). */
+typedef struct lsnif_profile {
+  uint64_t launches;
+  uint64_t trace_launches, mlp_launches;
+  double trace_ms, mlp_ms;
+} lsnif_profile;
+lsnif_status lsnif_profile_enable(lsnif_model model, int enable);
+lsnif_status lsnif_profile_read(lsnif_model model, void* stream, int reset, lsnif_profile* out);
+
 const char* lsnif_last_error(void);
 const char* lsnif_build_info(void);
 

@@ -95,7 +95,26 @@ struct Workspace {
   int32_t* counter = nullptr;
   unsigned long long* stats = nullptr;
   int64_t last_rays = 0;
+  // profiling: event pairs around each launch (kind 0 trace, 1 mlp)
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+  uint64_t launches[2] = {0, 0};
+  cudaEvent_t take_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+  }
   ~Workspace() {
+    for (auto& u : ev_used) {
+      cudaEventDestroy(u.second.first);
+      cudaEventDestroy(u.second.second);
+    }
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     cudaFree(X);
     cudaFree(meta);
     cudaFree(counter);
@@ -132,6 +151,7 @@ struct lsnif_model_s {
   std::map<cudaStream_t, std::unique_ptr<Workspace>> ws;
   std::unique_ptr<HostStaging> staging;
   std::mutex staging_mu;
+  bool profiling = false;
 
   ~lsnif_model_s() {
     cudaSetDevice(device);
@@ -351,6 +371,20 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
     }
   }
 
+  // Occlusion boundary: smallest float z with 1/(1+expf(-z)) > 0.5, found by
+  // bisection over the ordered bit patterns of [0, 1].
+  {
+    auto occ = [](float z) { return 1.0f / (1.0f + std::exp(-z)) > 0.5f; };
+    uint32_t lo = 0u, hi = 0x3f800000u;  // occ(0) false, occ(1) true
+    while (hi - lo > 1u) {
+      const uint32_t mid = lo + (hi - lo) / 2;
+      float z;
+      std::memcpy(&z, &mid, 4);
+      if (occ(z)) hi = mid; else lo = mid;
+    }
+    std::memcpy(&m.occ_threshold, &hi, 4);
+  }
+
   M.info.voxel_res = V;
   M.info.hit_cap = H;
   M.info.n_levels = L;
@@ -494,7 +528,18 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     tp.row_counter = w.counter;
     tp.stats = w.stats;
     tp.tile_bytes = M.tile_bytes();
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (M.profiling) {
+      e0 = w.take_event();
+      ck(cudaEventRecord(e0, st), "cudaEventRecord");
+    }
     ck(lsnif_dev::launch_trace(tp, false, st), "trace_encode_kernel");
+    ++w.launches[0];
+    if (M.profiling) {
+      e1 = w.take_event();
+      ck(cudaEventRecord(e1, st), "cudaEventRecord");
+      w.ev_used.push_back({0, {e0, e1}});
+    }
     lsnif_dev::MlpParams mp{};
     mp.m = M.dm;
     mp.X = w.X;
@@ -503,8 +548,18 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     mp.out = d_hits + s;
     mp.tile_bytes = M.tile_bytes();
     mp.mode = mode;
+    if (M.profiling) {
+      e0 = w.take_event();
+      ck(cudaEventRecord(e0, st), "cudaEventRecord");
+    }
     ck(lsnif_dev::launch_mlp(mp, static_cast<int>((cn + kTileM - 1) / kTileM), M.num_sms, st),
        "mlp_tc_kernel");
+    ++w.launches[1];
+    if (M.profiling) {
+      e1 = w.take_event();
+      ck(cudaEventRecord(e1, st), "cudaEventRecord");
+      w.ev_used.push_back({1, {e0, e1}});
+    }
   }
 }
 
@@ -640,6 +695,44 @@ lsnif_status lsnif_debug_traverse(lsnif_model model, const lsnif_ray* d_rays, in
     tp.hidx = hidx;
     tp.feat = feat;
     ck(lsnif_dev::launch_trace(tp, true, st), "trace_encode_kernel<debug>");
+  });
+}
+
+lsnif_status lsnif_profile_enable(lsnif_model model, int enable) {
+  return guarded([&] {
+    check_model(model);
+    model->profiling = enable != 0;
+  });
+}
+
+lsnif_status lsnif_profile_read(lsnif_model model, void* stream, int reset, lsnif_profile* out) {
+  return guarded([&] {
+    check_model(model);
+    if (!out) fail(LSNIF_INVALID_ARGUMENT, "null output");
+    ck(cudaSetDevice(model->device), "cudaSetDevice");
+    *out = lsnif_profile{};
+    std::lock_guard<std::mutex> lock(model->mu);
+    for (auto& kv : model->ws) {
+      if (stream && kv.first != static_cast<cudaStream_t>(stream)) continue;
+      Workspace& w = *kv.second;
+      ck(cudaStreamSynchronize(kv.first), "cudaStreamSynchronize");
+      out->trace_launches += w.launches[0];
+      out->mlp_launches += w.launches[1];
+      for (auto& u : w.ev_used) {
+        float ms = 0.0f;
+        ck(cudaEventElapsedTime(&ms, u.second.first, u.second.second), "cudaEventElapsedTime");
+        (u.first == 0 ? out->trace_ms : out->mlp_ms) += ms;
+      }
+      if (reset) {
+        for (auto& u : w.ev_used) {
+          w.ev_pool.push_back(u.second.first);
+          w.ev_pool.push_back(u.second.second);
+        }
+        w.ev_used.clear();
+        w.launches[0] = w.launches[1] = 0;
+      }
+    }
+    out->launches = out->trace_launches + out->mlp_launches;
   });
 }
 

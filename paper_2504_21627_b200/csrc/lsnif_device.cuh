@@ -41,6 +41,7 @@ struct DevModel {
   uint32_t w1_bytes, w2_bytes, w3_bytes;
   const float* w_f32;                  // w1 | b1 | w2 | b2 | w3 | b3 (decoded fp32, row-major)
   float act_scale, inv_act_scale;      // power of two
+  float occ_threshold;                 // smallest z with 1/(1+expf(-z)) > 0.5 under the host libm
   float z_zero[32];                    // logits of the all-zero input (rays without points)
 };
 
@@ -328,12 +329,15 @@ __device__ __forceinline__ float sigmoid_ref(float v) {
   return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-v)));
 }
 
-__device__ __forceinline__ void decode_hit(const float* z, int n_mat, float enter, float exit,
-                                           float t_min, float t_max, int mode, bool pair_flag,
-                                           lsnif_hit& h) {
-  const float occ = sigmoid_ref(z[0]);
+// The occlusion decision sigmoid(z0) > 0.5 (renderer.cpp:212) is monotone in
+// z0; it is taken as z0 >= occ_threshold, the boundary computed on the host
+// with the reference's (correctly rounded) expf, so it does not depend on the
+// last-ulp behaviour of the device expf.
+__device__ __forceinline__ void decode_hit(const float* z, int n_mat, float occ_threshold,
+                                           float enter, float exit, float t_min, float t_max,
+                                           int mode, bool pair_flag, lsnif_hit& h) {
   const float lt = sigmoid_ref(z[1]);
-  const bool occluded = occ > 0.5f;
+  const bool occluded = z[0] >= occ_threshold;
   const float tw = __fadd_rn(enter, __fmul_rn(lt, __fsub_rn(exit, enter)));
   const float n0 = z[2], n1 = z[3], n2 = z[4];
   const float len = sqrtf(__fadd_rn(__fadd_rn(__fmul_rn(n0, n0), __fmul_rn(n1, n1)), __fmul_rn(n2, n2)));

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(128) trace_encode_kernel(const TraceParams P) 
       store_hit(P.out + ray_idx, h);
     } else if (pair && count == 0) {
       lsnif_hit h;
-      decode_hit(m.z_zero, m.n_mat, enter, exit, t_min, t_max, P.mode, true, h);
+      decode_hit(m.z_zero, m.n_mat, m.occ_threshold, enter, exit, t_min, t_max, P.mode, true, h);
       store_hit(P.out + ray_idx, h);
     }
   } else if (live) {
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(128, 1) mlp_tc_kernel(const MlpParams P) {
           const float4 a = mp[0];
           const float4 b = mp[1];
           lsnif_hit h;
-          decode_hit(z, m.n_mat, a.y, a.z, a.w, b.x, P.mode, true, h);
+          decode_hit(z, m.n_mat, m.occ_threshold, a.y, a.z, a.w, b.x, P.mode, true, h);
           store_hit(P.out + __float_as_int(a.x), h);
         }
         tc::tc_fence_before();
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(128) infer_f32_kernel(const DevModel m, const 
     z[i] = __fadd_rn(s, b3[i]);
   }
   lsnif_hit h;
-  decode_hit(z, m.n_mat, iv[j].enter, iv[j].exit, 0.0f, 0.0f, LSNIF_QUERY_CLOSEST, false, h);
+  decode_hit(z, m.n_mat, m.occ_threshold, iv[j].enter, iv[j].exit, 0.0f, 0.0f, LSNIF_QUERY_CLOSEST, false, h);
   store_hit(out + j, h);
 }
 

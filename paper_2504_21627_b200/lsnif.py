@@ -44,6 +44,11 @@ class ModelInfo(C.Structure):
                 ("device_bytes", C.c_uint64)]
 
 
+class Profile(C.Structure):
+    _fields_ = [("launches", C.c_uint64), ("trace_launches", C.c_uint64),
+                ("mlp_launches", C.c_uint64), ("trace_ms", C.c_double), ("mlp_ms", C.c_double)]
+
+
 class QueryStats(C.Structure):
     _fields_ = [("rays", C.c_int64), ("pairs", C.c_int64), ("mlp_rows", C.c_int64),
                 ("points", C.c_int64), ("volume_points", C.c_int64)]
@@ -72,9 +77,11 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.lsnif_infer_batch.argtypes = [P, P, C.c_int64, C.c_int64, P, C.c_int64, P, P]
     lib.lsnif_debug_traverse.argtypes = [P, P, C.c_int64] + [P] * 7 + [P]
     lib.lsnif_last_query_stats.argtypes = [P, P, C.POINTER(QueryStats)]
+    lib.lsnif_profile_enable.argtypes = [P, C.c_int]
+    lib.lsnif_profile_read.argtypes = [P, P, C.c_int, C.POINTER(Profile)]
     for name in ("lsnif_model_load", "lsnif_model_destroy", "lsnif_model_get_info", "lsnif_query",
                  "lsnif_query_host", "lsnif_infer_batch", "lsnif_debug_traverse",
-                 "lsnif_last_query_stats"):
+                 "lsnif_last_query_stats", "lsnif_profile_enable", "lsnif_profile_read"):
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -146,6 +153,17 @@ class GpuModel:
         s = QueryStats()
         _check(load_library().lsnif_last_query_stats(self.h, _stream_ptr(stream), C.byref(s)))
         return {k: int(getattr(s, k)) for k, _ in QueryStats._fields_}
+
+    def profile_enable(self, enable: bool = True) -> None:
+        _check(load_library().lsnif_profile_enable(self.h, int(enable)))
+
+    def profile_read(self, reset: bool = True, stream=None) -> dict:
+        """Summed kernel durations / launch counts on `stream` (all streams if
+        stream == 'all')."""
+        p = Profile()
+        sp = None if stream == "all" else _stream_ptr(stream)
+        _check(load_library().lsnif_profile_read(self.h, sp, int(reset), C.byref(p)))
+        return {k: getattr(p, k) for k, _ in Profile._fields_}
 
     def debug_traverse(self, rays) -> dict:
         torch = _torch()

@@ -49,10 +49,19 @@ def counter_uniforms(seed: int, index: np.ndarray, k: int) -> np.ndarray:
     return out
 
 
+def rank_jitter(rank: int) -> tuple[float, float]:
+    """Sub-pixel sample position of a rank's frame: pixel centre for rank 0,
+    a low-discrepancy offset otherwise (each GPU answers a different frame)."""
+    if rank == 0:
+        return (0.5, 0.5)
+    return ((rank * 0.6180339887) % 1.0, (rank * 0.7548776662) % 1.0)
+
+
 def camera_rays(width: int, height: int, rows: tuple[int, int] | None = None,
-                camera: dict = CAMERA) -> np.ndarray:
-    """Pixel-centre pinhole rays in row-major pixel order (renderer.cpp:346-360).
-    `rows` = (y0, y1) selects a row band (for tile sharding)."""
+                camera: dict = CAMERA, jitter: tuple[float, float] = (0.5, 0.5)) -> np.ndarray:
+    """Pinhole rays in row-major pixel order (renderer.cpp:346-360) with the
+    sub-pixel sample at `jitter` (pixel centre by default). `rows` = (y0, y1)
+    selects a row band (for tile sharding)."""
     f32 = np.float32
     pos = np.array(camera["position"], f32)
     fwd = np.array(camera["look_at"], f32) - pos
@@ -65,8 +74,8 @@ def camera_rays(width: int, height: int, rows: tuple[int, int] | None = None,
     half_w = f32(half_h * f32(width) / f32(height))
     y0, y1 = rows if rows is not None else (0, height)
     py, px = np.meshgrid(np.arange(y0, y1, dtype=f32), np.arange(width, dtype=f32), indexing="ij")
-    sx = (f32(2) * (px + f32(0.5)) / f32(width) - f32(1)).reshape(-1, 1)
-    sy = (f32(1) - f32(2) * (py + f32(0.5)) / f32(height)).reshape(-1, 1)
+    sx = (f32(2) * (px + f32(jitter[0])) / f32(width) - f32(1)).reshape(-1, 1)
+    sy = (f32(1) - f32(2) * (py + f32(jitter[1])) / f32(height)).reshape(-1, 1)
     d = fwd + (sx * half_w) * right + (sy * half_h) * upv
     d = d / np.sqrt(np.sum(d * d, axis=1, keepdims=True, dtype=f32))
     rays = np.zeros(len(d), RAY_DTYPE)
