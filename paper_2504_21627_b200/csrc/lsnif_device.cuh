@@ -99,16 +99,6 @@ __device__ __forceinline__ bool frame_interval(const DevModel& m, const float o[
 
 // ------------------------------------------------------------------- DDA
 
-// State of one Amanatides-Woo walk (dda.cpp:40-117) in local unit-cube space.
-struct DdaState {
-  float o[3], d[3];
-  float t1;
-  float t_next[3], t_delta[3];
-  int cell[3];
-  int entry_axis;
-  float entry_t, entry_plane;
-};
-
 // dda.cpp:14-36 slab_interval
 __device__ __forceinline__ bool slab_interval(const float o[3], const float d[3], float t_min,
                                               float& t0, float& t1, int& enter_axis) {
@@ -139,181 +129,252 @@ __device__ __forceinline__ bool slab_interval(const float o[3], const float d[3]
   return true;
 }
 
-// dda.cpp:45-86: world->local (renderer.cpp:252-253), plane nudge, clip,
-// start cell and stepping constants. Returns false when the local ray misses.
-__device__ __forceinline__ bool dda_setup(const DevModel& m, const float wo[3], const float wd[3],
-                                          float t_min, DdaState& s) {
+// State of one Amanatides-Woo walk (dda.cpp:40-117) in local unit-cube space.
+// The current cell is the linear occupancy index `idx` (x fastest,
+// voxel.hpp:30-34) plus, per axis, the number of cells left before the walk
+// leaves the grid; V is a power of two, so cell coordinates are bit fields
+// of idx. The entry plane of a stepped-into cell is derived from the new cell
+// when a point is emitted (dda.cpp:108: c_old+1 == c_new for +steps, c_old for
+// -steps) instead of being tracked every step.
+struct Walk {
+  float o[3], d[3];    // nudged local origin and local direction
+  float t1;
+  float tn[3], td[3];  // t_next, t_delta
+  int rem[3];
+  int lin[3];          // linear-index increment of one step per axis
+  uint32_t idx;
+  float t0;
+  int axis0;           // entry axis of the start cell (-1: origin inside)
+  float plane0;        // entry plane of the start cell (dda.cpp:86)
+};
+
+// dda.cpp:45-86 (+ renderer.cpp:252-253 world->local): nudge, clip, start
+// cell and stepping constants. Returns false when the local ray misses.
+__device__ __forceinline__ bool walk_setup(const DevModel& m, int log2v, const float wo[3],
+                                           const float wd[3], float t_min, Walk& w) {
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    s.o[a] = __fmul_rn(__fsub_rn(wo[a], m.mn[a]), m.inv_ext[a]);
-    s.d[a] = __fmul_rn(wd[a], m.inv_ext[a]);
+    w.o[a] = __fmul_rn(__fsub_rn(wo[a], m.mn[a]), m.inv_ext[a]);
+    w.d[a] = __fmul_rn(wd[a], m.inv_ext[a]);
   }
   const float fres = m.fres;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {  // dda.cpp:49-53
-    const float scaled = __fmul_rn(s.o[a], fres);
-    if (scaled == floorf(scaled)) s.o[a] = __fadd_rn(s.o[a], 1e-7f);
+    const float scaled = __fmul_rn(w.o[a], fres);
+    if (scaled == floorf(scaled)) w.o[a] = __fadd_rn(w.o[a], 1e-7f);
   }
   float t0;
   int entry_axis;
-  if (!slab_interval(s.o, s.d, t_min, t0, s.t1, entry_axis)) return false;
+  if (!slab_interval(w.o, w.d, t_min, t0, w.t1, entry_axis)) return false;
   float start[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) start[a] = __fadd_rn(s.o[a], __fmul_rn(t0, s.d[a]));
+  for (int a = 0; a < 3; ++a) start[a] = __fadd_rn(w.o[a], __fmul_rn(t0, w.d[a]));
   const float inf = __int_as_float(0x7f800000);
+  uint32_t idx = 0;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {  // dda.cpp:64-79
     const int c = iclamp(static_cast<int>(floorf(__fmul_rn(start[a], fres))), 0, m.V - 1);
-    s.cell[a] = c;
-    const float da = s.d[a];
+    idx |= static_cast<uint32_t>(c) << (a * log2v);
+    const float da = w.d[a];
     if (da > 0.0f) {
-      s.t_delta[a] = __fdiv_rn(1.0f, __fmul_rn(fres, da));
+      w.td[a] = __fdiv_rn(1.0f, __fmul_rn(fres, da));
       // (c + 1) / fres is exact as a product by 1/fres (fres a power of two)
-      s.t_next[a] = __fadd_rn(t0, __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(c + 1), m.inv_fres),
-                                                      start[a]), da));
+      w.tn[a] = __fadd_rn(t0, __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(c + 1), m.inv_fres),
+                                                  start[a]), da));
+      w.rem[a] = m.V - 1 - c;
+      w.lin[a] = 1 << (a * log2v);
     } else if (da < 0.0f) {
-      s.t_delta[a] = __fdiv_rn(-1.0f, __fmul_rn(fres, da));
-      s.t_next[a] = __fadd_rn(t0, __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(c), m.inv_fres),
-                                                      start[a]), da));
+      w.td[a] = __fdiv_rn(-1.0f, __fmul_rn(fres, da));
+      w.tn[a] = __fadd_rn(t0, __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(c), m.inv_fres),
+                                                  start[a]), da));
+      w.rem[a] = c;
+      w.lin[a] = -(1 << (a * log2v));
     } else {
-      s.t_delta[a] = inf;
-      s.t_next[a] = inf;
+      w.td[a] = inf;
+      w.tn[a] = inf;
+      w.rem[a] = 1 << 30;
+      w.lin[a] = 0;
     }
   }
-  s.entry_t = t0;
-  s.entry_axis = entry_axis;
-  s.entry_plane = -1.0f;
+  w.idx = idx;
+  w.t0 = t0;
+  w.axis0 = entry_axis;
+  w.plane0 = -1.0f;
   if (entry_axis >= 0) {
     const float sa = entry_axis == 0 ? start[0] : entry_axis == 1 ? start[1] : start[2];
-    s.entry_plane = roundf(__fmul_rn(sa, fres));
+    w.plane0 = roundf(__fmul_rn(sa, fres));
   }
   return true;
 }
 
-__device__ __forceinline__ bool occ_test(const uint32_t* occ, int V, int x, int y, int z) {
-  const uint32_t i = static_cast<uint32_t>(x) + static_cast<uint32_t>(V) *
-                     (static_cast<uint32_t>(y) + static_cast<uint32_t>(V) * static_cast<uint32_t>(z));
-  return (occ[i >> 5] >> (i & 31)) & 1u;
+__device__ __forceinline__ bool occ_bit(const uint32_t* occ, uint32_t idx) {
+  return (occ[idx >> 5] >> (idx & 31)) & 1u;
 }
 
-// The entry point of the current cell (dda.cpp:90-95 + 113): o + entry_t*d
-// with the entry-axis coordinate snapped to entry_plane / V. The reference
-// computes entry_point at every step; it is a pure function of entry_t, so
-// it is evaluated only when emitted.
-__device__ __forceinline__ void dda_entry_point(const DdaState& s, float inv_fres, float p[3]) {
+// One advance (dda.cpp:103-115): argmin of t_next with ties to the lower
+// axis, stop when it exceeds t1 or the cell leaves the grid. On success
+// `t` is the entry parameter of the new cell and `axis` its entry axis.
+__device__ __forceinline__ bool walk_advance(Walk& w, float& t, int& axis) {
+  const bool p1 = w.tn[1] < w.tn[0];
+  float tn = p1 ? w.tn[1] : w.tn[0];
+  const bool p2 = w.tn[2] < tn;
+  tn = p2 ? w.tn[2] : tn;
+  if (tn > w.t1) return false;
+  const bool a0 = !p1 && !p2;
+  const bool a1 = p1 && !p2;
+  if (a0) { w.tn[0] = __fadd_rn(w.tn[0], w.td[0]); w.rem[0] -= 1; w.idx += w.lin[0]; }
+  if (a1) { w.tn[1] = __fadd_rn(w.tn[1], w.td[1]); w.rem[1] -= 1; w.idx += w.lin[1]; }
+  if (p2) { w.tn[2] = __fadd_rn(w.tn[2], w.td[2]); w.rem[2] -= 1; w.idx += w.lin[2]; }
+  if ((w.rem[0] | w.rem[1] | w.rem[2]) < 0) return false;
+  t = tn;
+  axis = p2 ? 2 : (p1 ? 1 : 0);
+  return true;
+}
+
+// Entry plane (in grid units) of the cell `idx` entered along `axis`.
+__device__ __forceinline__ float walk_plane(const Walk& w, int log2v, int V, int axis) {
+  const int c = static_cast<int>(w.idx >> (axis * log2v)) & (V - 1);
+  const float da = axis == 0 ? w.d[0] : axis == 1 ? w.d[1] : w.d[2];
+  return static_cast<float>(da > 0.0f ? c : c + 1);
+}
+
+// Pool entry of one boundary point: entry t and (axis | plane << 2), axis 3
+// marking the origin-inside start point (first_is_origin).
+__device__ __forceinline__ uint2 pack_point(float t, int axis, float plane) {
+  const uint32_t code = axis < 0 ? 3u : (static_cast<uint32_t>(axis) | (static_cast<uint32_t>(plane) << 2));
+  return make_uint2(__float_as_uint(t), code);
+}
+
+// Entry point of a pooled boundary point (dda.cpp:90-95, 113): o + t*d with
+// the entry-axis coordinate snapped to plane / V.
+__device__ __forceinline__ void unpack_point(uint2 e, const float o[3], const float d[3],
+                                             float inv_fres, float p[3], bool& volume) {
+  const float t = __uint_as_float(e.x);
+  const uint32_t axis = e.y & 3u;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) p[a] = __fadd_rn(s.o[a], __fmul_rn(s.entry_t, s.d[a]));
-  if (s.entry_axis >= 0) {
-    const float snapped = __fmul_rn(s.entry_plane, inv_fres);  // == entry_plane / fres
-    if (s.entry_axis == 0) p[0] = snapped;
-    else if (s.entry_axis == 1) p[1] = snapped;
-    else p[2] = snapped;
-  }
-}
-
-// One advance (dda.cpp:103-115). Returns false when the walk ends.
-__device__ __forceinline__ bool dda_advance(DdaState& s, int V) {
-  int axis = 0;
-  float tn = s.t_next[0];
-  if (s.t_next[1] < tn) { axis = 1; tn = s.t_next[1]; }
-  if (s.t_next[2] < tn) { axis = 2; tn = s.t_next[2]; }
-  if (tn > s.t1) return false;
-  s.entry_t = tn;
-  const float da = axis == 0 ? s.d[0] : axis == 1 ? s.d[1] : s.d[2];
-  const int ca = axis == 0 ? s.cell[0] : axis == 1 ? s.cell[1] : s.cell[2];
-  const int step = da > 0.0f ? 1 : -1;  // t_next finite implies d != 0
-  s.entry_plane = static_cast<float>(step > 0 ? ca + 1 : ca);
-  const int nc = ca + step;
-  if (nc < 0 || nc >= V) return false;
-  s.entry_axis = axis;
-  if (axis == 0) { s.cell[0] = nc; s.t_next[0] = __fadd_rn(s.t_next[0], s.t_delta[0]); }
-  else if (axis == 1) { s.cell[1] = nc; s.t_next[1] = __fadd_rn(s.t_next[1], s.t_delta[1]); }
-  else { s.cell[2] = nc; s.t_next[2] = __fadd_rn(s.t_next[2], s.t_delta[2]); }
-  return true;
+  for (int a = 0; a < 3; ++a) p[a] = __fadd_rn(o[a], __fmul_rn(t, d[a]));
+  volume = axis == 3u;
+  const float snapped = __fmul_rn(static_cast<float>(e.y >> 2), inv_fres);  // == plane / fres
+  if (axis == 0u) p[0] = snapped;
+  else if (axis == 1u) p[1] = snapped;
+  else if (axis == 2u) p[2] = snapped;
 }
 
 // ---------------------------------------------------------------- encode
 
-// hash_vertex (encoding.hpp:18-23)
-__device__ __forceinline__ uint32_t hash_vertex(const DevModel& m, int x, int y, int z) {
-  const uint32_t h = static_cast<uint32_t>(x) ^ static_cast<uint32_t>(y) * 2654435761u ^
-                     static_cast<uint32_t>(z) * 805459861u;
+constexpr uint32_t kP1 = 2654435761u, kP2 = 805459861u;  // encoding.hpp:19-21
+
+// hash_vertex (encoding.hpp:18-23) reduction
+template <bool POW2>
+__device__ __forceinline__ uint32_t hash_reduce(const DevModel& m, uint32_t h) {
+  if (POW2) return h & m.M_mask;
   return m.M_pow2 ? (h & m.M_mask) : (h % m.M);
 }
 
 __device__ __forceinline__ void unpack4(uint2 e, float f[4]) {
-  const __half2 a = *reinterpret_cast<const __half2*>(&e.x);
-  const __half2 b = *reinterpret_cast<const __half2*>(&e.y);
-  f[0] = __low2float(a);
-  f[1] = __high2float(a);
-  f[2] = __low2float(b);
-  f[3] = __high2float(b);
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&e.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&e.y));
+  f[0] = a.x;
+  f[1] = a.y;
+  f[2] = b.x;
+  f[3] = b.y;
 }
 
-// encode_point_level (encoding.hpp:84-140): features[f] for one point on one
-// level, fp32 accumulation in corner order 0..7. `hidx` (nullable) receives
-// the hashed indices in visit order (debug probe).
-__device__ __forceinline__ void encode_point_level(const DevModel& m, int level, const float p[3],
-                                                   bool volume, float feat[4], uint32_t* hidx) {
+// The interpolation plane axis of a boundary point (encoding.hpp:95-108):
+// argmin_a |p_a V - round(p_a V)| with the first minimum winning. The
+// entry-axis coordinate is an exact multiple of 1/V (distance 0, the global
+// minimum), so the argmin is the first axis whose p_a * V is an integer.
+__device__ __forceinline__ int plane_axis_of(const float p[3], float fv) {
+  const float s0 = __fmul_rn(p[0], fv), s1 = __fmul_rn(p[1], fv);
+  return (s0 == rintf(s0)) ? 0 : (s1 == rintf(s1)) ? 1 : 2;
+}
+
+// encode_point_level (encoding.hpp:84-140) for a boundary point: the 4
+// in-plane corners. With the plane axis a and free axes b < c, the
+// reference's corner order (dx,dy,dz bits, skipping the +1 side of a) is
+// (db,dc) = (0,0),(1,0),(0,1),(1,1) and its weight wx*wy*wz = wb*wc exactly
+// (the plane factor is 1 - 0). F <= 4 features, fp32 accumulation.
+template <bool POW2>
+__device__ __forceinline__ void encode_boundary_level(const DevModel& m, int level, const float p[3],
+                                                      int pa, float feat[4], uint32_t* hidx) {
   const int res = m.level_res[level];
   const float fres = static_cast<float>(res);
-  float u[3];
+  const int b = pa == 0 ? 1 : 0;
+  const int c = pa == 2 ? 1 : 2;
+  const float pa_v = pa == 0 ? p[0] : pa == 1 ? p[1] : p[2];
+  const float pb_v = b == 0 ? p[0] : p[1];
+  const float pc_v = c == 1 ? p[1] : p[2];
+  const int base_a = iclamp(static_cast<int>(roundf(__fmul_rn(pa_v, fres))), 0, res);
+  const float ub = __fmul_rn(pb_v, fres), uc = __fmul_rn(pc_v, fres);
+  const int base_b = iclamp(static_cast<int>(floorf(ub)), 0, res - 1);
+  const int base_c = iclamp(static_cast<int>(floorf(uc)), 0, res - 1);
+  const float fb = fclamp(__fsub_rn(ub, static_cast<float>(base_b)), 0.0f, 1.0f);
+  const float fc = fclamp(__fsub_rn(uc, static_cast<float>(base_c)), 0.0f, 1.0f);
+  const uint32_t Pa = pa == 0 ? 1u : pa == 1 ? kP1 : kP2;
+  const uint32_t Pb = b == 0 ? 1u : kP1;
+  const uint32_t Pc = c == 1 ? kP1 : kP2;
+  const uint32_t ha = static_cast<uint32_t>(base_a) * Pa;
+  const uint32_t hb0 = static_cast<uint32_t>(base_b) * Pb, hb1 = hb0 + Pb;
+  const uint32_t hc0 = static_cast<uint32_t>(base_c) * Pc, hc1 = hc0 + Pc;
+  uint32_t idx[4];
+  idx[0] = hash_reduce<POW2>(m, ha ^ hb0 ^ hc0);
+  idx[1] = hash_reduce<POW2>(m, ha ^ hb1 ^ hc0);
+  idx[2] = hash_reduce<POW2>(m, ha ^ hb0 ^ hc1);
+  idx[3] = hash_reduce<POW2>(m, ha ^ hb1 ^ hc1);
+  const uint2* table = m.tables[level];
+  uint2 ent[4];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) u[a] = __fmul_rn(p[a], fres);
-  int plane_axis = -1;
-  if (!volume) {
-    float best = 3.402823466e38f;
-    const float fv = static_cast<float>(m.V);
+  for (int k = 0; k < 4; ++k) ent[k] = __ldg(table + idx[k]);
+  if (hidx) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const float scaled = __fmul_rn(p[a], fv);
-      const float dist = fabsf(__fsub_rn(scaled, roundf(scaled)));
-      if (dist < best) {
-        best = dist;
-        plane_axis = a;
-      }
-    }
+    for (int k = 0; k < 4; ++k) hidx[k] = idx[k];
   }
+  const float wb0 = __fsub_rn(1.0f, fb), wc0 = __fsub_rn(1.0f, fc);
+  const float w[4] = {__fmul_rn(wb0, wc0), __fmul_rn(fb, wc0), __fmul_rn(wb0, fc), __fmul_rn(fb, fc)};
+  feat[0] = feat[1] = feat[2] = feat[3] = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    float t[4];
+    unpack4(ent[k], t);
+#pragma unroll
+    for (int f = 0; f < 4; ++f) feat[f] = __fadd_rn(feat[f], __fmul_rn(w[k], t[f]));
+  }
+}
+
+// Volume fallback (first point of a ray starting inside an occupied cell):
+// all 8 corners, trilinear (encoding.hpp:109-139 with plane_axis = -1).
+template <bool POW2>
+__device__ __forceinline__ void encode_volume_level(const DevModel& m, int level, const float p[3],
+                                                    float feat[4], uint32_t* hidx) {
+  const int res = m.level_res[level];
+  const float fres = static_cast<float>(res);
   int base[3];
   float frac[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    if (a == plane_axis) {
-      base[a] = iclamp(static_cast<int>(roundf(u[a])), 0, res);
-      frac[a] = 0.0f;
-    } else {
-      base[a] = iclamp(static_cast<int>(floorf(u[a])), 0, res - 1);
-      frac[a] = fclamp(__fsub_rn(u[a], static_cast<float>(base[a])), 0.0f, 1.0f);
-    }
+    const float u = __fmul_rn(p[a], fres);
+    base[a] = iclamp(static_cast<int>(floorf(u)), 0, res - 1);
+    frac[a] = fclamp(__fsub_rn(u, static_cast<float>(base[a])), 0.0f, 1.0f);
   }
   const uint2* table = m.tables[level];
-  // Issue all gathers first (up to 8 independent 8-byte loads in flight).
   uint2 ent[8];
   float w[8];
-  int cnt = 0;
 #pragma unroll
   for (int corner = 0; corner < 8; ++corner) {
     const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
-    const bool skip = (plane_axis == 0 && dx) || (plane_axis == 1 && dy) || (plane_axis == 2 && dz);
     const float wx = dx ? frac[0] : __fsub_rn(1.0f, frac[0]);
     const float wy = dy ? frac[1] : __fsub_rn(1.0f, frac[1]);
     const float wz = dz ? frac[2] : __fsub_rn(1.0f, frac[2]);
     w[corner] = __fmul_rn(__fmul_rn(wx, wy), wz);
-    const uint32_t idx = hash_vertex(m, base[0] + dx, base[1] + dy, base[2] + dz);
-    if (!skip) {
-      ent[corner] = __ldg(table + idx);
-      if (hidx) hidx[cnt] = idx;
-      ++cnt;
-    } else {
-      ent[corner] = make_uint2(0u, 0u);
-    }
+    const uint32_t h = static_cast<uint32_t>(base[0] + dx) ^ static_cast<uint32_t>(base[1] + dy) * kP1 ^
+                       static_cast<uint32_t>(base[2] + dz) * kP2;
+    const uint32_t idx = hash_reduce<POW2>(m, h);
+    ent[corner] = __ldg(table + idx);
+    if (hidx) hidx[corner] = idx;
   }
   feat[0] = feat[1] = feat[2] = feat[3] = 0.0f;
 #pragma unroll
   for (int corner = 0; corner < 8; ++corner) {
-    const int dx = corner & 1, dy = (corner >> 1) & 1, dz = (corner >> 2) & 1;
-    const bool skip = (plane_axis == 0 && dx) || (plane_axis == 1 && dy) || (plane_axis == 2 && dz);
-    if (skip) continue;
     float t[4];
     unpack4(ent[corner], t);
 #pragma unroll

@@ -23,186 +23,207 @@ namespace lsnif_dev {
 
 // ======================================================= trace + encode
 
-template <bool DEBUG>
-__global__ void __launch_bounds__(128) trace_encode_kernel(const TraceParams P) {
+// Persistent: each block loads the occupancy bitset once and loops over
+// 128-ray batches. Per warp: DDA per lane (points -> 8-byte pool entries),
+// then a warp-cooperative encode of all pooled points. LS/FS: compile-time
+// level/feature counts (0 = read from the model); POW2: M is a power of two.
+template <bool DEBUG, int LS, int FS, bool POW2>
+__global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   const DevModel& m = P.m;
-  const int occ_words = (m.V * m.V * m.V) >> 5;
+  const int L = LS ? LS : m.L;
+  const int F = FS ? FS : m.F;
+  const int LF = L * F;
+  const int H = m.H;
+  const int V = m.V;
+  const int log2v = __ffs(V) - 1;
+  const int occ_words = (V * V * V) >> 5;
   for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.occ + i);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  float4* pool = reinterpret_cast<float4*>(smem + ((occ_words + 3) & ~3)) + warp * (m.H * 32);
+  uint2* pool = reinterpret_cast<uint2*>(smem + ((occ_words + 3) & ~3)) + warp * (H * 32);
   __syncthreads();
-
-  const int64_t ray_idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool live = ray_idx < P.n;
-  float o[3] = {0, 0, 0}, d[3] = {0, 0, 0}, t_min = 0.0f, t_max = 0.0f;
-  if (live) {
-    const float4* r4 = reinterpret_cast<const float4*>(P.rays + ray_idx);
-    const float4 a = __ldg(r4), b = __ldg(r4 + 1);
-    o[0] = a.x; o[1] = a.y; o[2] = a.z;
-    d[0] = a.w; d[1] = b.x; d[2] = b.y;
-    t_min = b.z; t_max = b.w;
-  }
-  float enter = 0.0f, exit = 0.0f;
-  const bool pair = live && frame_interval(m, o, d, t_min, t_max, enter, exit);
-
-  // ---- DDA: occupied-cell entry points into this lane's pool column
-  int count = 0;
-  bool fio = false;
-  if (pair) {
-    DdaState s;
-    if (dda_setup(m, o, d, t_min, s)) {
-      while (true) {
-        if (occ_test(smem, m.V, s.cell[0], s.cell[1], s.cell[2])) {
-          float p[3];
-          dda_entry_point(s, m.inv_fres, p);
-          if (s.entry_axis < 0 && count == 0) fio = true;
-          pool[count * 32 + lane] = make_float4(p[0], p[1], p[2], s.entry_t);
-          if (DEBUG)
-            P.cells[ray_idx * m.H + count] = static_cast<uint32_t>(s.cell[0]) |
-                                             static_cast<uint32_t>(s.cell[1]) << 8 |
-                                             static_cast<uint32_t>(s.cell[2]) << 16;
-          ++count;
-          if (count >= m.H) break;
-        }
-        if (!dda_advance(s, m.V)) break;
-      }
-    }
-  }
-
-  // ---- rays answered without the MLP
-  if (!DEBUG) {
-    if (live && !pair) {
-      lsnif_hit h{};
-      store_hit(P.out + ray_idx, h);
-    } else if (pair && count == 0) {
-      lsnif_hit h;
-      decode_hit(m.z_zero, m.n_mat, m.occ_threshold, enter, exit, t_min, t_max, P.mode, true, h);
-      store_hit(P.out + ray_idx, h);
-    }
-  } else if (live) {
-    P.info[ray_idx] = pair ? (count | (fio ? 1 << 8 : 0) | (1 << 9)) : 0;
-    P.interval[2 * ray_idx] = pair ? enter : 0.0f;
-    P.interval[2 * ray_idx + 1] = pair ? exit : 0.0f;
-  }
-
-  // ---- row allocation (warp-aggregated) for rays that need the MLP
-  const bool valid = pair && count > 0;
-  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-  const unsigned lt_mask = (1u << lane) - 1u;
-  int row = 0;
-  if (!DEBUG) {
-    int base = 0;
-    if (lane == 0 && vmask) base = atomicAdd(P.row_counter, __popc(vmask));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    row = base + __popc(vmask & lt_mask);
-    if (valid) {
-      RowMeta rm;
-      rm.ray = static_cast<int32_t>(ray_idx);
-      rm.enter = enter;
-      rm.exit = exit;
-      rm.t_min = t_min;
-      rm.t_max = t_max;
-      rm.pad[0] = rm.pad[1] = rm.pad[2] = 0;
-      float4* dst = reinterpret_cast<float4*>(P.meta + row);
-      dst[0] = make_float4(__int_as_float(rm.ray), rm.enter, rm.exit, rm.t_min);
-      dst[1] = make_float4(rm.t_max, 0.0f, 0.0f, 0.0f);
-    }
-    // query statistics (pairs, MLP rows, points, volume points)
-    const int n_pair = __popc(__ballot_sync(0xffffffffu, pair));
-    const int n_pts = __reduce_add_sync(0xffffffffu, valid ? count : 0);
-    const int n_vol = __popc(__ballot_sync(0xffffffffu, valid && fio));
-    if (lane == 0 && n_pair) {
-      atomicAdd(P.stats + 0, static_cast<unsigned long long>(n_pair));
-      atomicAdd(P.stats + 1, static_cast<unsigned long long>(__popc(vmask)));
-      atomicAdd(P.stats + 2, static_cast<unsigned long long>(n_pts));
-      atomicAdd(P.stats + 3, static_cast<unsigned long long>(n_vol));
-    }
-  }
-
-  // ---- warp-cooperative encode of all pooled points
-  const int c = valid ? count : 0;
-  int incl = c;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const int v = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += v;
-  }
-  const int excl = incl - c;
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
-  const unsigned fio_mask = __ballot_sync(0xffffffffu, valid && fio);
   const float scale = m.act_scale;
-  const int LF = m.LF, F = m.F;
-  for (int jb = 0; jb < total; jb += 32) {
-    const int j = jb + lane;
-    int owner = 0;
-#pragma unroll
-    for (int step = 16; step >= 1; step >>= 1) {
-      const int ex = __shfl_sync(0xffffffffu, excl, owner + step);
-      if (ex <= j) owner += step;
-    }
-    const int o_excl = __shfl_sync(0xffffffffu, excl, owner);
-    const int o_row = __shfl_sync(0xffffffffu, row, owner);
-    const long long o_ray = __shfl_sync(0xffffffffu, static_cast<long long>(ray_idx), owner);
-    if (j >= total) continue;
-    const int k = j - o_excl;
-    const float4 pp = pool[k * 32 + owner];
-    const float p[3] = {pp.x, pp.y, pp.z};
-    const bool volume = (k == 0) && ((fio_mask >> owner) & 1u);
-    float fv[16];
-    for (int l = 0; l < m.L; ++l) {
-      float feat[4];
-      uint32_t hidx[8];
-      encode_point_level(m, l, p, volume, feat, DEBUG ? hidx : nullptr);
-      if (DEBUG) {
-        const int64_t hb = ((o_ray * m.H + k) * m.L + l) * 8;
-        const int nc = volume ? 8 : 4;
-        for (int q = 0; q < nc; ++q) P.hidx[hb + q] = hidx[q];
-        for (int f = 0; f < F; ++f) P.feat[o_ray * m.K1 + k * LF + l * F + f] = feat[f];
-      }
-#pragma unroll
-      for (int f = 0; f < 4; ++f)
-        if (f < F) fv[l * F + f] = feat[f];
-    }
-    if (DEBUG) {
-      P.t[o_ray * m.H + k] = pp.w;
-      P.pts[(o_ray * m.H + k) * 3 + 0] = pp.x;
-      P.pts[(o_ray * m.H + k) * 3 + 1] = pp.y;
-      P.pts[(o_ray * m.H + k) * 3 + 2] = pp.z;
-    } else {
-      uint8_t* tile = P.X + static_cast<int64_t>(o_row >> 7) * P.tile_bytes;
-      const int r = o_row & 127;
-      const int col0 = k * LF;
-      if ((LF & 1) == 0) {
-        for (int q = 0; q < LF; q += 2) {
-          const __half2 hv = __floats2half2_rn(__fmul_rn(fv[q], scale), __fmul_rn(fv[q + 1], scale));
-          *reinterpret_cast<__half2*>(tile + canon_offset(r, col0 + q, kTileM)) = hv;
-        }
-      } else {
-        for (int q = 0; q < LF; ++q)
-          *reinterpret_cast<__half*>(tile + canon_offset(r, col0 + q, kTileM)) =
-              __float2half_rn(__fmul_rn(fv[q], scale));
-      }
-    }
-  }
+  const int64_t nbatch = (P.n + 127) / 128;
 
-  // ---- zero padding of the row tail + bias constant column (encoding.hpp:170)
-  if (!DEBUG && valid) {
-    uint8_t* tile = P.X + static_cast<int64_t>(row >> 7) * P.tile_bytes;
-    const int r = row & 127;
-    const __half hs = __float2half_rn(scale);
-    const __half hz = __float2half_rn(0.0f);
-    int col = count * LF;
-    for (; col < m.K1P && (col & 7); ++col)
-      *reinterpret_cast<__half*>(tile + canon_offset(r, col, kTileM)) = (col == m.K1) ? hs : hz;
-    for (; col < m.K1P; col += 8) {
-      __align__(16) __half v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = (col + q == m.K1) ? hs : hz;
-      *reinterpret_cast<uint4*>(tile + canon_offset(r, col, kTileM)) =
-          *reinterpret_cast<const uint4*>(v);
+  for (int64_t batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
+    const int64_t ray_idx = batch * 128 + threadIdx.x;
+    const bool live = ray_idx < P.n;
+    float o[3] = {0, 0, 0}, d[3] = {0, 0, 0}, t_min = 0.0f, t_max = 0.0f;
+    if (live) {
+      const float4* r4 = reinterpret_cast<const float4*>(P.rays + ray_idx);
+      const float4 ra = __ldg(r4), rb = __ldg(r4 + 1);
+      o[0] = ra.x; o[1] = ra.y; o[2] = ra.z;
+      d[0] = ra.w; d[1] = rb.x; d[2] = rb.y;
+      t_min = rb.z; t_max = rb.w;
     }
+    float enter = 0.0f, exit = 0.0f;
+    const bool pair = live && frame_interval(m, o, d, t_min, t_max, enter, exit);
+
+    // ---- DDA (dda.cpp:88-116): occupied-cell entry points into the pool
+    Walk w;
+    int count = 0;
+    bool fio = false;
+    if (pair && walk_setup(m, log2v, o, d, t_min, w)) {
+      if (occ_bit(smem, w.idx)) {
+        fio = w.axis0 < 0;
+        pool[lane] = pack_point(w.t0, w.axis0, w.plane0);
+        if (DEBUG) P.cells[ray_idx * H] = (w.idx & (V - 1)) | ((w.idx >> log2v) & (V - 1)) << 8 |
+                                          ((w.idx >> (2 * log2v)) & (V - 1)) << 16;
+        count = 1;
+      }
+      float t;
+      int axis;
+      while (count < H && walk_advance(w, t, axis)) {
+        if (occ_bit(smem, w.idx)) {
+          pool[count * 32 + lane] = pack_point(t, axis, walk_plane(w, log2v, V, axis));
+          if (DEBUG)
+            P.cells[ray_idx * H + count] = (w.idx & (V - 1)) | ((w.idx >> log2v) & (V - 1)) << 8 |
+                                           ((w.idx >> (2 * log2v)) & (V - 1)) << 16;
+          ++count;
+        }
+      }
+    }
+
+    // ---- rays answered without the MLP
+    if (!DEBUG) {
+      if (live && !pair) {
+        lsnif_hit h{};
+        store_hit(P.out + ray_idx, h);
+      } else if (pair && count == 0) {
+        lsnif_hit h;
+        decode_hit(m.z_zero, m.n_mat, m.occ_threshold, enter, exit, t_min, t_max, P.mode, true, h);
+        store_hit(P.out + ray_idx, h);
+      }
+    } else if (live) {
+      P.info[ray_idx] = pair ? (count | (fio ? 1 << 8 : 0) | (1 << 9)) : 0;
+      P.interval[2 * ray_idx] = pair ? enter : 0.0f;
+      P.interval[2 * ray_idx + 1] = pair ? exit : 0.0f;
+    }
+
+    // ---- row allocation (warp-aggregated) for rays that need the MLP
+    const bool valid = pair && count > 0;
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    int row = 0;
+    if (!DEBUG) {
+      int base = 0;
+      if (lane == 0 && vmask) base = atomicAdd(P.row_counter, __popc(vmask));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      row = base + __popc(vmask & ((1u << lane) - 1u));
+      if (valid) {
+        float4* dst = reinterpret_cast<float4*>(P.meta + row);
+        dst[0] = make_float4(__int_as_float(static_cast<int32_t>(ray_idx)), enter, exit, t_min);
+        dst[1] = make_float4(t_max, 0.0f, 0.0f, 0.0f);
+      }
+      const int n_pair = __popc(__ballot_sync(0xffffffffu, pair));
+      const int n_pts = __reduce_add_sync(0xffffffffu, valid ? count : 0);
+      const int n_vol = __popc(__ballot_sync(0xffffffffu, valid && fio));
+      if (lane == 0 && n_pair) {
+        atomicAdd(P.stats + 0, static_cast<unsigned long long>(n_pair));
+        atomicAdd(P.stats + 1, static_cast<unsigned long long>(__popc(vmask)));
+        atomicAdd(P.stats + 2, static_cast<unsigned long long>(n_pts));
+        atomicAdd(P.stats + 3, static_cast<unsigned long long>(n_vol));
+      }
+    }
+
+    // ---- warp-cooperative encode of all pooled points (encoding.hpp:166-176)
+    const int c = valid ? count : 0;
+    int incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    const int excl = incl - c;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int jb = 0; jb < total; jb += 32) {
+      const int j = jb + lane;
+      int owner = 0;
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1) {
+        const int ex = __shfl_sync(0xffffffffu, excl, owner + st);
+        if (ex <= j) owner += st;
+      }
+      const int o_excl = __shfl_sync(0xffffffffu, excl, owner);
+      const int o_row = __shfl_sync(0xffffffffu, row, owner);
+      float ro[3], rd[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        ro[a] = __shfl_sync(0xffffffffu, w.o[a], owner);
+        rd[a] = __shfl_sync(0xffffffffu, w.d[a], owner);
+      }
+      const int64_t o_ray = batch * 128 + warp * 32 + owner;
+      if (j >= total) continue;
+      const int k = j - o_excl;
+      const uint2 e = pool[k * 32 + owner];
+      float p[3];
+      bool volume;
+      unpack_point(e, ro, rd, m.inv_fres, p, volume);
+      float fv[16];
+      const int pa = volume ? -1 : plane_axis_of(p, m.fres);
+#pragma unroll
+      for (int l = 0; l < (LS ? LS : kMaxLevels); ++l) {
+        if (!LS && l >= L) break;
+        float feat[4];
+        uint32_t hidx[8];
+        if (volume)
+          encode_volume_level<POW2>(m, l, p, feat, DEBUG ? hidx : nullptr);
+        else
+          encode_boundary_level<POW2>(m, l, p, pa, feat, DEBUG ? hidx : nullptr);
+        if (DEBUG) {
+          const int64_t hb = ((o_ray * H + k) * L + l) * 8;
+          const int nc = volume ? 8 : 4;
+          for (int q = 0; q < nc; ++q) P.hidx[hb + q] = hidx[q];
+          for (int f = 0; f < F; ++f) P.feat[o_ray * m.K1 + k * LF + l * F + f] = feat[f];
+        }
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+          if (f < F) fv[l * F + f] = feat[f];
+      }
+      if (DEBUG) {
+        P.t[o_ray * H + k] = __uint_as_float(e.x);
+        P.pts[(o_ray * H + k) * 3 + 0] = p[0];
+        P.pts[(o_ray * H + k) * 3 + 1] = p[1];
+        P.pts[(o_ray * H + k) * 3 + 2] = p[2];
+      } else {
+        uint8_t* tile = P.X + static_cast<int64_t>(o_row >> 7) * P.tile_bytes;
+        const int r = o_row & 127;
+        const int col0 = k * LF;
+        if ((LF & 1) == 0) {
+#pragma unroll
+          for (int q = 0; q < (LS && FS ? LS * FS : 16); q += 2) {
+            if (!(LS && FS) && q >= LF) break;
+            const __half2 hv = __floats2half2_rn(__fmul_rn(fv[q], scale), __fmul_rn(fv[q + 1], scale));
+            *reinterpret_cast<__half2*>(tile + canon_offset(r, col0 + q, kTileM)) = hv;
+          }
+        } else {
+          for (int q = 0; q < LF; ++q)
+            *reinterpret_cast<__half*>(tile + canon_offset(r, col0 + q, kTileM)) =
+                __float2half_rn(__fmul_rn(fv[q], scale));
+        }
+      }
+    }
+
+    // ---- zero padding of the row tail + bias constant column (encoding.hpp:170)
+    if (!DEBUG && valid) {
+      uint8_t* tile = P.X + static_cast<int64_t>(row >> 7) * P.tile_bytes;
+      const int r = row & 127;
+      const __half hs = __float2half_rn(scale);
+      const __half hz = __float2half_rn(0.0f);
+      int col = count * LF;
+      for (; col < m.K1P && (col & 7); ++col)
+        *reinterpret_cast<__half*>(tile + canon_offset(r, col, kTileM)) = (col == m.K1) ? hs : hz;
+      for (; col < m.K1P; col += 8) {
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        const int q = m.K1 - col;
+        if (q >= 0 && q < 8) {
+          const uint32_t hbits = static_cast<uint32_t>(__half_as_ushort(hs)) << ((q & 1) * 16);
+          if (q < 2) v.x = hbits; else if (q < 4) v.y = hbits; else if (q < 6) v.z = hbits; else v.w = hbits;
+        }
+        *reinterpret_cast<uint4*>(tile + canon_offset(r, col, kTileM)) = v;
+      }
+    }
+    __syncwarp();  // pool reuse by the next batch
   }
 }
 
@@ -406,7 +427,7 @@ __global__ void __launch_bounds__(128) infer_f32_kernel(const DevModel m, const 
 
 size_t trace_smem_bytes(const DevModel& m) {
   const size_t occ_words = (static_cast<size_t>(m.V) * m.V * m.V) >> 5;
-  return ((occ_words + 3) & ~size_t(3)) * 4 + 4 * static_cast<size_t>(m.H) * 32 * 16;
+  return ((occ_words + 3) & ~size_t(3)) * 4 + 4 * static_cast<size_t>(m.H) * 32 * 8;
 }
 
 size_t mlp_smem_bytes(const DevModel& m) {
@@ -414,20 +435,28 @@ size_t mlp_smem_bytes(const DevModel& m) {
   return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + xh + 64;
 }
 
+template <bool DEBUG, int LS, int FS, bool POW2>
+static cudaError_t launch_trace_t(const TraceParams& p, cudaStream_t st) {
+  auto kern = trace_encode_kernel<DEBUG, LS, FS, POW2>;
+  const size_t smem = trace_smem_bytes(p.m);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem);
+  const int64_t nbatch = (p.n + 127) / 128;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nbatch, static_cast<int64_t>(sms) * std::max(per_sm, 1)));
+  kern<<<grid, 128, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st) {
   if (p.n <= 0) return cudaSuccess;
-  const size_t smem = trace_smem_bytes(p.m);
-  const unsigned blocks = static_cast<unsigned>((p.n + 127) / 128);
-  if (debug) {
-    cudaFuncSetAttribute(trace_encode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    trace_encode_kernel<true><<<blocks, 128, smem, st>>>(p);
-  } else {
-    cudaFuncSetAttribute(trace_encode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
-    trace_encode_kernel<false><<<blocks, 128, smem, st>>>(p);
-  }
-  return cudaGetLastError();
+  const bool fast = p.m.L == 2 && p.m.F == 3 && p.m.M_pow2;
+  if (debug) return fast ? launch_trace_t<true, 2, 3, true>(p, st) : launch_trace_t<true, 0, 0, false>(p, st);
+  return fast ? launch_trace_t<false, 2, 3, true>(p, st) : launch_trace_t<false, 0, 0, false>(p, st);
 }
 
 cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st) {
