@@ -7,7 +7,11 @@ NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
            -Xcompiler -fPIC -Xcompiler -ffp-contract=off -Xptxas -v \
            -Iinclude -I$(PKG)/csrc
 
-all: $(PKG)/liblsnif_gpu.so oracle
+all: $(PKG)/liblsnif_gpu.so oracle examples/query_cpp
+
+examples/query_cpp: examples/query_cpp.cpp include/lsnif_gpu.hpp include/lsnif_gpu.h $(PKG)/liblsnif_gpu.so
+	g++ -std=c++17 -O2 -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -llsnif_gpu \
+	    -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,/usr/local/cuda/lib64
 
 $(PKG)/liblsnif_gpu.so: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC) 2> build_ptxas.log || (cat build_ptxas.log; false)
@@ -17,7 +21,7 @@ oracle:
 	$(MAKE) -s -C oracle all
 
 clean:
-	rm -f $(PKG)/liblsnif_gpu.so build_ptxas.log
+	rm -f $(PKG)/liblsnif_gpu.so build_ptxas.log examples/query_cpp
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle clean

@@ -1,0 +1,150 @@
+// lsnif_gpu.hpp — header-only C++ host adapter over the C ABI (lsnif_gpu.h).
+//
+// Re-declares (does not copy) the reference's query surface
+// (proj/include/lsnif/renderer.hpp:42-53, 110-116) so a caller of the CPU
+// narrow phase can switch to the B200 path:
+//   lsnif::gpu::Model            ~ std::shared_ptr<const LsnifModel> + upload
+//   lsnif::gpu::infer_batch      ~ infer_batch (renderer.hpp:52-53)
+//   lsnif::gpu::intersect        ~ the narrow phase + accept of intersect_scene
+//                                  for one object (renderer.cpp:269-303)
+//   lsnif::gpu::occluded_batch   ~ occluded_batch (renderer.cpp:305-323)
+// Errors are rethrown as the reference's exception types:
+// std::invalid_argument for LSNIF_INVALID_ARGUMENT, std::runtime_error
+// otherwise.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "lsnif_gpu.h"
+
+namespace lsnif {
+namespace gpu {
+
+inline void check(lsnif_status st) {
+  if (st == LSNIF_OK) return;
+  const std::string msg = lsnif_last_error();
+  if (st == LSNIF_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+// renderer.hpp:42-48
+struct NeuralHit {
+  bool occluded = false;
+  float t_world = 0;
+  float normal[3] = {0, 0, 0};
+  float albedo[3] = {0, 0, 0};
+  int material_index = 0;
+};
+
+inline NeuralHit to_neural_hit(const lsnif_hit& h) {
+  NeuralHit n;
+  n.occluded = (h.flags_material & LSNIF_HIT_OCCLUDED) != 0;
+  n.t_world = h.t_world;
+  for (int k = 0; k < 3; ++k) {
+    n.normal[k] = h.normal[k];
+    n.albedo[k] = h.albedo[k];
+  }
+  n.material_index = static_cast<int>(h.flags_material >> LSNIF_HIT_MATERIAL_SHIFT);
+  return n;
+}
+
+// A device-resident model; copies share the device upload (the reference
+// shares one immutable LsnifModel across instances, renderer.cpp:55-76).
+class Model {
+ public:
+  static Model load(const std::string& path, int device = 0) {
+    lsnif_model m = nullptr;
+    check(lsnif_model_load(path.c_str(), device, &m));
+    return Model(m);
+  }
+  static Model create(const lsnif_model_desc& desc, int device = 0) {
+    lsnif_model m = nullptr;
+    check(lsnif_model_create(&desc, device, &m));
+    return Model(m);
+  }
+  lsnif_model handle() const { return h_.get(); }
+  lsnif_model_info info() const {
+    lsnif_model_info i{};
+    check(lsnif_model_get_info(h_.get(), &i));
+    return i;
+  }
+  int input_width() const {
+    const lsnif_model_info i = info();
+    return i.hit_cap * i.n_levels * i.f_dim;
+  }
+
+ private:
+  explicit Model(lsnif_model m) : h_(m, [](lsnif_model p) { lsnif_model_destroy(p); }) {}
+  std::shared_ptr<lsnif_model_s> h_;
+};
+
+// Device buffer helper (RAII).
+template <typename T>
+struct DeviceBuffer {
+  T* ptr = nullptr;
+  explicit DeviceBuffer(size_t n) {
+    if (n && cudaMalloc(&ptr, n * sizeof(T)) != cudaSuccess) throw std::runtime_error("cudaMalloc failed");
+  }
+  ~DeviceBuffer() { cudaFree(ptr); }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+};
+
+// infer_batch (renderer.cpp:183-226): `inputs` is MatX inputs(input_width, n)
+// in column-major order, one interval per column.
+inline std::vector<NeuralHit> infer_batch(const Model& model, const std::vector<float>& inputs,
+                                          const std::vector<lsnif_interval>& intervals) {
+  const int64_t rows = model.input_width();
+  const int64_t n = rows ? static_cast<int64_t>(inputs.size()) / rows : 0;
+  if (n * rows != static_cast<int64_t>(inputs.size()))
+    throw std::invalid_argument("infer_batch: input width mismatch");
+  DeviceBuffer<float> dx(inputs.size());
+  DeviceBuffer<lsnif_interval> di(intervals.size());
+  DeviceBuffer<lsnif_hit> dh(static_cast<size_t>(n));
+  if (!inputs.empty()) cudaMemcpy(dx.ptr, inputs.data(), inputs.size() * 4, cudaMemcpyHostToDevice);
+  if (!intervals.empty())
+    cudaMemcpy(di.ptr, intervals.data(), intervals.size() * sizeof(lsnif_interval), cudaMemcpyHostToDevice);
+  check(lsnif_infer_batch(model.handle(), dx.ptr, rows, n, di.ptr, static_cast<int64_t>(intervals.size()),
+                          dh.ptr, nullptr));
+  std::vector<lsnif_hit> raw(static_cast<size_t>(n));
+  if (n) cudaMemcpy(raw.data(), dh.ptr, raw.size() * sizeof(lsnif_hit), cudaMemcpyDeviceToHost);
+  std::vector<NeuralHit> out;
+  out.reserve(raw.size());
+  for (const lsnif_hit& h : raw) out.push_back(to_neural_hit(h));
+  return out;
+}
+
+// One query per ray (object-space rays), results in ray order.
+inline std::vector<lsnif_hit> query(const Model& model, const std::vector<lsnif_ray>& rays, int mode) {
+  std::vector<lsnif_hit> hits(rays.size());
+  check(lsnif_query_host(model.handle(), rays.data(), static_cast<int64_t>(rays.size()), mode, hits.data(),
+                         nullptr));
+  return hits;
+}
+
+// Closest-hit narrow phase of intersect_scene for one LSNIF object at identity
+// transform: the accepted neural hit per ray, if any.
+inline std::vector<std::optional<NeuralHit>> intersect(const Model& model, const std::vector<lsnif_ray>& rays) {
+  const std::vector<lsnif_hit> hits = query(model, rays, LSNIF_QUERY_CLOSEST);
+  std::vector<std::optional<NeuralHit>> out(hits.size());
+  for (size_t i = 0; i < hits.size(); ++i)
+    if (hits[i].flags_material & LSNIF_HIT_ACCEPTED) out[i] = to_neural_hit(hits[i]);
+  return out;
+}
+
+// occluded_batch (renderer.cpp:305-323) for one LSNIF object.
+inline std::vector<char> occluded_batch(const Model& model, const std::vector<lsnif_ray>& rays) {
+  const std::vector<lsnif_hit> hits = query(model, rays, LSNIF_QUERY_ANY);
+  std::vector<char> out(hits.size(), 0);
+  for (size_t i = 0; i < hits.size(); ++i) out[i] = (hits[i].flags_material & LSNIF_HIT_ACCEPTED) ? 1 : 0;
+  return out;
+}
+
+}  // namespace gpu
+}  // namespace lsnif

@@ -117,7 +117,6 @@ struct Workspace {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
     cudaFree(X);
     cudaFree(meta);
-    cudaFree(counter);
     cudaFree(stats);
   }
 };
@@ -138,6 +137,8 @@ struct HostStaging {
 
 constexpr int64_t kChunk = int64_t(1) << 21;      // rays per trace/MLP launch pair
 constexpr int64_t kHostChunk = int64_t(1) << 20;  // rays per host staging step
+constexpr size_t kMaxChunks = 1024;                // row counters per query (2^31 rays)
+constexpr size_t kCounterBytes = 32 + 4 * kMaxChunks;
 
 }  // namespace
 
@@ -175,8 +176,10 @@ struct lsnif_model_s {
     auto& slot = ws[st];
     if (!slot) {
       slot = std::make_unique<Workspace>();
-      ck(cudaMalloc(&slot->counter, 64), "cudaMalloc(counter)");
-      ck(cudaMalloc(&slot->stats, 64), "cudaMalloc(stats)");
+      // one allocation, reset by a single memset per query: stats (4 x u64)
+      // followed by one row counter per chunk
+      ck(cudaMalloc(&slot->stats, kCounterBytes), "cudaMalloc(counters)");
+      slot->counter = reinterpret_cast<int32_t*>(slot->stats + 4);
     }
     Workspace& w = *slot;
     const int64_t rows = std::min<int64_t>(n, kChunk);
@@ -512,11 +515,11 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
   if (n > INT32_MAX) fail(LSNIF_INVALID_ARGUMENT, "more than 2^31-1 rays in one call");
   ck(cudaSetDevice(M.device), "cudaSetDevice");
   Workspace& w = M.workspace(st, std::max<int64_t>(n, 1));
-  ck(cudaMemsetAsync(w.stats, 0, 64, st), "cudaMemsetAsync");
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  ck(cudaMemsetAsync(w.stats, 0, 32 + 4 * static_cast<size_t>(nchunks), st), "cudaMemsetAsync");
   w.last_rays = n;
-  for (int64_t s = 0; s < n; s += kChunk) {
+  for (int64_t s = 0, ci = 0; s < n; s += kChunk, ++ci) {
     const int64_t cn = std::min(kChunk, n - s);
-    ck(cudaMemsetAsync(w.counter, 0, 4, st), "cudaMemsetAsync");
     lsnif_dev::TraceParams tp{};
     tp.m = M.dm;
     tp.rays = d_rays + s;
@@ -525,7 +528,7 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     tp.out = d_hits + s;
     tp.X = w.X;
     tp.meta = w.meta;
-    tp.row_counter = w.counter;
+    tp.row_counter = w.counter + ci;
     tp.stats = w.stats;
     tp.tile_bytes = M.tile_bytes();
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -544,7 +547,7 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     mp.m = M.dm;
     mp.X = w.X;
     mp.meta = w.meta;
-    mp.row_counter = w.counter;
+    mp.row_counter = w.counter + ci;
     mp.out = d_hits + s;
     mp.tile_bytes = M.tile_bytes();
     mp.mode = mode;

@@ -229,49 +229,103 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
 
 // ============================================================ tcgen05 MLP
 
-// Shared-memory plan (bytes, all 1024-aligned): W1 | W2 | W3 | XH | bars.
+// Warp-specialised persistent MLP over the compacted 128-row X tiles:
+//   warp 0  loader: bulk-copies X tiles into a 2-stage SMEM ring;
+//   warp 1  MMA issuer (one thread) + TMEM allocator;
+//   warps 2-5 / 6-9  two epilogue groups, ping-ponging over tiles, each with
+//           its own TMEM accumulator (128 lanes x HID cols) and SMEM hidden
+//           operand buffer, so one tile's epilogue overlaps the other's MMAs.
+// Per tile: L1 = X W1^T (+b1 via the constant column), h1 = leaky(.) -> SMEM,
+// L2, h2 -> SMEM, L3 (N = 16), heads/decode/accept -> global hits.
 template <int HID>
-struct MlpSmem {
-  static constexpr int kK2 = HID + 16;                 // hidden + bias block
-  static constexpr int kXHBytes = kTileM * kK2 * 2;    // holds X (K1P <= K2) or H
+struct MlpLayout {
+  static constexpr int kK2 = HID + 16;                      // hidden + bias block
+  static constexpr uint32_t kHBytes = kTileM * kK2 * 2;     // hidden operand buffer
+  static constexpr int kThreads = 320;
 };
 
+__device__ __forceinline__ void leaky_store8(const uint32_t* acc, uint8_t* dst) {
+  __align__(16) __half2 hv[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    float v0 = __uint_as_float(acc[2 * e]);
+    float v1 = __uint_as_float(acc[2 * e + 1]);
+    v0 = fmaxf(v0, __fmul_rn(v0, 0.01f));
+    v1 = fmaxf(v1, __fmul_rn(v1, 0.01f));
+    hv[e] = __floats2half2_rn(v0, v1);
+  }
+  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(hv);
+}
+
+// h = leaky(acc) -> fp16 hidden operand row. The bias is already accumulated
+// and the activation scale carries through the positively homogeneous
+// leaky-ReLU. TMEM loads are issued two at a time (64 columns in flight).
 template <int HID>
-__global__ void __launch_bounds__(128, 1) mlp_tc_kernel(const MlpParams P) {
+__device__ __forceinline__ void epi_hidden(uint32_t taddr, uint8_t* sH, int row) {
+#pragma unroll
+  for (int cb = 0; cb < HID; cb += 64) {
+    uint32_t a0[32], a1[32];
+    tc::tmem_ld32(taddr + cb, a0);
+    tc::tmem_ld32(taddr + cb + 32, a1);
+    tc::tmem_wait_ld();
+#pragma unroll
+    for (int q = 0; q < 32; q += 8) leaky_store8(a0 + q, sH + canon_offset(row, cb + q, kTileM));
+#pragma unroll
+    for (int q = 0; q < 32; q += 8) leaky_store8(a1 + q, sH + canon_offset(row, cb + 32 + q, kTileM));
+  }
+}
+
+template <int HID>
+__global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(const MlpParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  using Lay = MlpLayout<HID>;
+  constexpr int K2 = Lay::kK2;
   const DevModel& m = P.m;
-  constexpr int K2 = MlpSmem<HID>::kK2;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t xbytes = static_cast<uint32_t>(kTileM) * m.K1P * 2;
+  const uint32_t xstage = (xbytes + 1023) & ~1023u;
   uint8_t* sW1 = base;
   uint8_t* sW2 = sW1 + m.w1_bytes;
   uint8_t* sW3 = sW2 + m.w2_bytes;
-  uint8_t* sXH = sW3 + ((m.w3_bytes + 1023) & ~1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sXH + MlpSmem<HID>::kXHBytes);
-  uint64_t* bar_load = bars;
-  uint64_t* bar_mma = bars + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+  uint8_t* sX = sW3 + ((m.w3_bytes + 1023) & ~1023u);
+  uint8_t* sH = sX + 2 * xstage;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * Lay::kHBytes);
+  uint64_t* w_full = bars;          // 1
+  uint64_t* x_full = bars + 1;      // 2
+  uint64_t* x_empty = bars + 3;     // 2
+  uint64_t* l_done = bars + 5;      // 2
+  uint64_t* h_ready = bars + 7;     // 2
+  uint64_t* acc_free = bars + 9;    // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
 
   const int rows = *P.row_counter;
   const int ntiles = (rows + kTileM - 1) / kTileM;
   if (static_cast<int>(blockIdx.x) >= ntiles) return;
+  const int my_tiles = (ntiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                       static_cast<int>(gridDim.x);
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  const int lane = tid & 31;
   if (tid == 0) {
-    tc::mbar_init(bar_load, 1);
-    tc::mbar_init(bar_mma, 1);
+    tc::mbar_init(w_full, 1);
+    for (int g = 0; g < 2; ++g) {
+      tc::mbar_init(x_full + g, 1);
+      tc::mbar_init(x_empty + g, 1);
+      tc::mbar_init(l_done + g, 1);
+      tc::mbar_init(h_ready + g, 128);
+      tc::mbar_init(acc_free + g, 128);
+    }
     tc::fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc(tmem_slot, HID);  // D reused by the three layers
-  // Bias block of the hidden operand: column HID = act_scale, HID+1..K2-1 = 0.
-  {
-    const __half hs = __float2half_rn(m.act_scale);
-    const __half hz = __float2half_rn(0.0f);
-    __align__(16) __half v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = q == 0 ? hs : hz;
-    *reinterpret_cast<uint4*>(sXH + canon_offset(tid, HID, kTileM)) = *reinterpret_cast<const uint4*>(v);
-    *reinterpret_cast<uint4*>(sXH + canon_offset(tid, HID + 8, kTileM)) = make_uint4(0, 0, 0, 0);
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * HID);
+  if (warp >= 2) {  // bias block of both hidden buffers: col HID = act_scale, rest 0
+    const int row = 32 * (warp & 3) + lane;
+    const int g = (warp - 2) >> 2;
+    const uint32_t hs = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(m.act_scale)));
+    uint8_t* h = sH + g * Lay::kHBytes;
+    *reinterpret_cast<uint4*>(h + canon_offset(row, HID, kTileM)) = make_uint4(hs, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(h + canon_offset(row, HID + 8, kTileM)) = make_uint4(0u, 0u, 0u, 0u);
   }
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
@@ -279,107 +333,117 @@ __global__ void __launch_bounds__(128, 1) mlp_tc_kernel(const MlpParams P) {
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (tid == 0) {
-    tc::mbar_arrive_expect_tx(bar_load, m.w1_bytes + m.w2_bytes + m.w3_bytes);
-    tc::bulk_g2s(sW1, m.w_canon, m.w1_bytes, bar_load);
-    tc::bulk_g2s(sW2, m.w_canon + m.w1_bytes, m.w2_bytes, bar_load);
-    tc::bulk_g2s(sW3, m.w_canon + m.w1_bytes + m.w2_bytes, m.w3_bytes, bar_load);
-  }
-  uint32_t load_phase = 0, mma_phase = 0;
-  tc::mbar_wait(bar_load, load_phase);
-  load_phase ^= 1;
-
-  const uint32_t x_bytes = static_cast<uint32_t>(kTileM) * m.K1P * 2;
-  const uint32_t sXH_a = tc::smem_addr(sXH);
-  const uint32_t sW1_a = tc::smem_addr(sW1), sW2_a = tc::smem_addr(sW2), sW3_a = tc::smem_addr(sW3);
-  constexpr uint32_t kIdescH = tc::idesc_f16_f32(kTileM, HID);
-  const uint32_t idesc3 = tc::idesc_f16_f32(kTileM, m.N3);
-  const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-  const uint32_t a_lbo = kTileM * 16;  // K-chunk stride of the 128-row A operand
-
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    // ---- X tile -> SMEM
-    if (tid == 0) {
-      tc::mbar_arrive_expect_tx(bar_load, x_bytes);
-      tc::bulk_g2s(sXH, P.X + static_cast<int64_t>(tile) * P.tile_bytes, x_bytes, bar_load);
-    }
-    tc::mbar_wait(bar_load, load_phase);
-    load_phase ^= 1;
-
-    // ---- three layers; hidden epilogues write back into sXH
-#pragma unroll 1
-    for (int layer = 0; layer < 3; ++layer) {
-      if (tid == 0) {
-        tc::tc_fence_after();
-        const int ksteps = (layer == 0 ? m.K1P : K2) / 16;
-        const uint32_t b_base = layer == 0 ? sW1_a : layer == 1 ? sW2_a : sW3_a;
-        const uint32_t b_rows = layer == 2 ? m.N3 : HID;
-        const uint32_t idesc = layer == 2 ? idesc3 : kIdescH;
-        for (int ks = 0; ks < ksteps; ++ks) {
-          const uint64_t ad = tc::smem_desc(sXH_a + ks * 2 * a_lbo, a_lbo, 128);
-          const uint64_t bd = tc::smem_desc(b_base + ks * 2 * b_rows * 16, b_rows * 16, 128);
-          tc::mma_f16_ss(tmem, ad, bd, idesc, ks > 0 ? 1u : 0u);
-        }
-        tc::mma_commit(bar_mma);
+  if (warp == 0) {
+    // ------------------------------------------------------------ loader
+    if (lane == 0) {
+      tc::mbar_arrive_expect_tx(w_full, m.w1_bytes + m.w2_bytes + m.w3_bytes);
+      tc::bulk_g2s(sW1, m.w_canon, m.w1_bytes, w_full);
+      tc::bulk_g2s(sW2, m.w_canon + m.w1_bytes, m.w2_bytes, w_full);
+      tc::bulk_g2s(sW3, m.w_canon + m.w1_bytes + m.w2_bytes, m.w3_bytes, w_full);
+      for (int i = 0; i < my_tiles; ++i) {
+        const int tile = blockIdx.x + i * gridDim.x;
+        const int st = i & 1, k = i >> 1;
+        if (k > 0) tc::mbar_wait(x_empty + st, (k - 1) & 1);
+        tc::mbar_arrive_expect_tx(x_full + st, xbytes);
+        tc::bulk_g2s(sX + st * xstage, P.X + static_cast<int64_t>(tile) * P.tile_bytes, xbytes, x_full + st);
       }
-      tc::mbar_wait(bar_mma, mma_phase);
-      mma_phase ^= 1;
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      tc::mbar_wait(w_full, 0);
+      const uint32_t sW1_a = tc::smem_addr(sW1), sW2_a = tc::smem_addr(sW2), sW3_a = tc::smem_addr(sW3);
+      constexpr uint32_t kIdescH = tc::idesc_f16_f32(kTileM, HID);
+      const uint32_t idesc3 = tc::idesc_f16_f32(kTileM, m.N3);
+      constexpr uint32_t a_lbo = kTileM * 16;
+      uint32_t hcount[2] = {0, 0};
+      auto layer = [&](uint32_t a_base, int ksteps, uint32_t b_base, uint32_t b_rows, uint32_t idesc,
+                       uint32_t d) {
+        tc::tc_fence_after();
+        for (int ks = 0; ks < ksteps; ++ks) {
+          const uint64_t ad = tc::smem_desc(a_base + ks * 2 * a_lbo, a_lbo, 128);
+          const uint64_t bd = tc::smem_desc(b_base + ks * 2 * b_rows * 16, b_rows * 16, 128);
+          tc::mma_f16_ss(d, ad, bd, idesc, ks > 0 ? 1u : 0u);
+        }
+      };
+      for (int i0 = 0; i0 < my_tiles; i0 += 2) {
+        const int n2 = min(2, my_tiles - i0);
+        for (int j = 0; j < n2; ++j) {  // L1 for both tiles of the pair
+          const int i = i0 + j, g = i & 1, k = i >> 1;
+          tc::mbar_wait(x_full + g, k & 1);
+          if (k > 0) tc::mbar_wait(acc_free + g, (k - 1) & 1);
+          layer(tc::smem_addr(sX + g * xstage), m.K1P / 16, sW1_a, HID, kIdescH, tmem + g * HID);
+          tc::mma_commit(x_empty + g);
+          tc::mma_commit(l_done + g);
+        }
+        for (int j = 0; j < n2; ++j) {  // L2
+          const int g = (i0 + j) & 1;
+          tc::mbar_wait(h_ready + g, hcount[g]++ & 1);
+          layer(tc::smem_addr(sH + g * Lay::kHBytes), K2 / 16, sW2_a, HID, kIdescH, tmem + g * HID);
+          tc::mma_commit(l_done + g);
+        }
+        for (int j = 0; j < n2; ++j) {  // L3
+          const int g = (i0 + j) & 1;
+          tc::mbar_wait(h_ready + g, hcount[g]++ & 1);
+          layer(tc::smem_addr(sH + g * Lay::kHBytes), K2 / 16, sW3_a, m.N3, idesc3, tmem + g * HID);
+          tc::mma_commit(l_done + g);
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogues
+    const int g = (warp - 2) >> 2;
+    const int row = 32 * (warp & 3) + lane;
+    const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + g * HID;
+    uint8_t* h = sH + g * Lay::kHBytes;
+    uint32_t lcount = 0;
+    for (int i = g; i < my_tiles; i += 2) {
+      const int tile = blockIdx.x + i * gridDim.x;
+      const int grow = tile * kTileM + row;
+      float4 ma = make_float4(0, 0, 0, 0), mb = ma;  // row metadata, prefetched
+      if (grow < rows) {
+        const float4* mp = reinterpret_cast<const float4*>(P.meta + grow);
+        ma = __ldg(mp);
+        mb = __ldg(mp + 1);
+      }
+      // layer 1 -> h1
+      tc::mbar_wait(l_done + g, lcount++ & 1);
       tc::tc_fence_after();
-
-      if (layer < 2) {
-        // h = leaky(acc) (bias already accumulated; the activation scale
-        // carries through the positively homogeneous leaky-ReLU)
+      epi_hidden<HID>(taddr, h, row);
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      tc::mbar_arrive(h_ready + g);
+      // layer 2 -> h2
+      tc::mbar_wait(l_done + g, lcount++ & 1);
+      tc::tc_fence_after();
+      epi_hidden<HID>(taddr, h, row);
+      tc::fence_proxy_async_smem();
+      tc::tc_fence_before();
+      tc::mbar_arrive(h_ready + g);
+      // layer 3 -> heads, decode, accept (renderer.cpp:208-223, 280-301)
+      tc::mbar_wait(l_done + g, lcount++ & 1);
+      tc::tc_fence_after();
+      float z[16];
+      {
+        uint32_t acc[16];
+        tc::tmem_ld16(taddr, acc);
+        tc::tmem_wait_ld();
 #pragma unroll
-        for (int cb = 0; cb < HID; cb += 32) {
-          uint32_t acc[32];
-          tc::tmem_ld32(tmem + lane_base + cb, acc);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int q = 0; q < 32; q += 8) {
-            __align__(16) __half2 hv[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float v0 = __uint_as_float(acc[q + 2 * e]);
-              float v1 = __uint_as_float(acc[q + 2 * e + 1]);
-              v0 = fmaxf(v0, __fmul_rn(v0, 0.01f));
-              v1 = fmaxf(v1, __fmul_rn(v1, 0.01f));
-              hv[e] = __floats2half2_rn(v0, v1);
-            }
-            *reinterpret_cast<uint4*>(sXH + canon_offset(tid, cb + q, kTileM)) =
-                *reinterpret_cast<const uint4*>(hv);
-          }
-        }
-        tc::fence_proxy_async_smem();
-        tc::tc_fence_before();
-        __syncthreads();
-      } else {
-        // ---- heads + decode + accept (renderer.cpp:208-223, 280-301)
-        const int row = tile * kTileM + tid;
-        float z[32];
-        for (int cb = 0; cb < m.N3; cb += 16) {
-          uint32_t acc[16];
-          tc::tmem_ld16(tmem + lane_base + cb, acc);
-          tc::tmem_wait_ld();
-#pragma unroll
-          for (int q = 0; q < 16; ++q) z[cb + q] = __fmul_rn(__uint_as_float(acc[q]), m.inv_act_scale);
-        }
-        if (row < rows) {
-          const float4* mp = reinterpret_cast<const float4*>(P.meta + row);
-          const float4 a = mp[0];
-          const float4 b = mp[1];
-          lsnif_hit h;
-          decode_hit(z, m.n_mat, m.occ_threshold, a.y, a.z, a.w, b.x, P.mode, true, h);
-          store_hit(P.out + __float_as_int(a.x), h);
-        }
-        tc::tc_fence_before();
-        __syncthreads();
+        for (int q = 0; q < 16; ++q) z[q] = __fmul_rn(__uint_as_float(acc[q]), m.inv_act_scale);
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(acc_free + g);
+      if (grow < rows) {
+        lsnif_hit hh;
+        decode_hit(z, m.n_mat, m.occ_threshold, ma.y, ma.z, ma.w, mb.x, P.mode, true, hh);
+        store_hit(P.out + __float_as_int(ma.x), hh);
       }
     }
   }
   __syncthreads();
-  if (warp == 0) {
+  if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, HID);
+    tc::tmem_dealloc(tmem, 2 * HID);
   }
 }
 
@@ -431,8 +495,9 @@ size_t trace_smem_bytes(const DevModel& m) {
 }
 
 size_t mlp_smem_bytes(const DevModel& m) {
-  const size_t xh = static_cast<size_t>(kTileM) * (m.hidden + 16) * 2;
-  return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + xh + 64;
+  const size_t h = static_cast<size_t>(kTileM) * (m.hidden + 16) * 2;
+  const size_t x = (static_cast<size_t>(kTileM) * m.K1P * 2 + 1023) & ~size_t(1023);
+  return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + 2 * x + 2 * h + 128;
 }
 
 template <bool DEBUG, int LS, int FS, bool POW2>
@@ -462,14 +527,13 @@ cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st) {
 cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st) {
   if (max_tiles <= 0) return cudaSuccess;
   const size_t smem = mlp_smem_bytes(p.m);
-  const int ctas_per_sm = smem <= 113 * 1024 ? 2 : 1;
-  const unsigned grid = static_cast<unsigned>(std::min(max_tiles, num_sms * ctas_per_sm));
+  const unsigned grid = static_cast<unsigned>(std::min(max_tiles, num_sms));
   if (p.m.hidden == 128) {
     cudaFuncSetAttribute(mlp_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    mlp_tc_kernel<128><<<grid, 128, smem, st>>>(p);
+    mlp_tc_kernel<128><<<grid, MlpLayout<128>::kThreads, smem, st>>>(p);
   } else {
     cudaFuncSetAttribute(mlp_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    mlp_tc_kernel<64><<<grid, 128, smem, st>>>(p);
+    mlp_tc_kernel<64><<<grid, MlpLayout<64>::kThreads, smem, st>>>(p);
   }
   return cudaGetLastError();
 }

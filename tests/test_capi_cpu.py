@@ -1,0 +1,86 @@
+"""CPU-only checks of the product boundary: the in-tree liblsnif_gpu.so loads
+without a GPU, exports every entry point include/lsnif_gpu.h declares, fails
+loudly (status + message, no crash) where a GPU or a valid file is needed,
+and the host-side workload generators are deterministic and shardable."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2504_21627_b200 import lsnif, workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "lsnif_gpu.h")).read()
+    return sorted(set(re.findall(r"\b(lsnif_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = lsnif.load_library()
+    syms = header_symbols()
+    assert len(syms) >= 12
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_struct_layouts_match_reference_records():
+    assert lsnif.RAY_DTYPE.itemsize == 32   # lsnif::Ray
+    assert lsnif.HIT_DTYPE.itemsize == 32
+    assert ctypes.sizeof(lsnif.QueryStats) == 40
+
+
+def test_errors_without_gpu_or_file(tmp_path):
+    lib = lsnif.load_library()
+    h = ctypes.c_void_p()
+    st = lib.lsnif_model_load(b"/nonexistent/model.lsnif", 0, ctypes.byref(h))
+    assert st == lsnif.RUNTIME_ERROR
+    assert b"cannot open model file" in lib.lsnif_last_error()
+    bad = tmp_path / "bad.lsnif"
+    bad.write_bytes(b"NOPE" + b"\0" * 64)
+    st = lib.lsnif_model_load(str(bad).encode(), 0, ctypes.byref(h))
+    assert st == lsnif.RUNTIME_ERROR and b"bad magic" in lib.lsnif_last_error()
+    st = lib.lsnif_query(None, None, 0, 0, None, None)
+    assert st == lsnif.INVALID_ARGUMENT
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    with pytest.raises(lsnif.LsnifError):
+        lsnif._lib_backup = lsnif._lib
+        try:
+            lsnif._lib = None
+            lsnif.load_library(str(tmp_path / "nope.so"))
+        finally:
+            lsnif._lib = lsnif._lib_backup
+
+
+def test_incoherent_generator_is_index_addressable():
+    box = np.array([-1, -1, -1, 1, 1, 1], np.float32)
+    full = W.incoherent_rays(1000, box, seed=3)
+    part = W.incoherent_rays(300, box, seed=3, start=500)
+    assert full[500:800].tobytes() == part.tobytes()
+    assert np.all((full["o"] >= box[:3]) & (full["o"] <= box[3:]))
+    assert np.allclose(np.linalg.norm(full["d"], axis=1), 1, atol=1e-5)
+
+
+def test_camera_row_bands_tile_the_frame():
+    from paper_2504_21627_b200.dist import row_band
+    full = W.camera_rays(64, 37)
+    parts = [W.camera_rays(64, 37, rows=row_band(37, 3, r)) for r in range(3)]
+    assert np.concatenate(parts).tobytes() == full.tobytes()
+
+
+def test_shadow_rays_point_at_light():
+    prim = W.camera_rays(8, 8)
+    hits = np.zeros(len(prim), lsnif.HIT_DTYPE)
+    hits["flags_material"][::3] = 7
+    hits["t_world"] = 4.0
+    hits["normal"] = (0, 1, 0)
+    box = np.array([-1, 0, -1, 1, 1, 1], np.float32)
+    rays, owner = W.shadow_rays(prim, hits, box)
+    assert len(rays) == len(owner) and np.all(owner % 3 == 0)
+    p_end = rays["o"] + rays["t_max"][:, None] / (1 - 1e-4) * rays["d"]
+    assert np.allclose(p_end, W.LIGHT, atol=1e-3)
