@@ -44,6 +44,9 @@ WORKLOADS = {
     "c3": "C3 (configs[2]): teapot LSNIF, 16,777,216 incoherent rays (origins uniform in "
           "the frame box, directions uniform on S^2, seed 3), closest-hit, per GPU",
     "c1": "C1 (configs[0]): teapot LSNIF, 256x256 pixel-centre primary rays, closest-hit",
+    "c5": "C5 (configs[4]): teapot LSNIF, 3840x2160 x 16 spp incoherent rays (132,710,400, "
+          "keyed by (pixel, sample)), closest-hit, row bands tile-sharded across the GPUs with "
+          "an NCCL result gather to rank 0 inside the step (strong scaling)",
 }
 
 
@@ -57,14 +60,20 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=6.0,
                     help="target CPU work per timed baseline pass")
+    ap.add_argument("--dist-backend", default=os.environ.get("LSNIF_DIST_BACKEND", "nccl"),
+                    help="nccl (one GPU per rank) or gloo (test mode: all ranks on cuda:0)")
     return ap.parse_args()
 
 
 # ----------------------------------------------------------------- workload
 
-def build_rays(workload: str, rank: int, box: np.ndarray):
-    """Returns [(rays, mode)] for one rank, before shadow generation."""
+def build_rays(workload: str, rank: int, box: np.ndarray, world: int = 1):
+    """Primary rays of one rank (before shadow generation)."""
     from paper_2504_21627_b200 import workloads as W
+    from paper_2504_21627_b200.dist import ray_range
+    if workload == "c5":
+        s, e = ray_range(3840 * 2160 * 16, world, rank)
+        return W.incoherent_rays(e - s, box, seed=5, start=s)
     if workload == "c2":
         return W.camera_rays(1920, 1080, jitter=W.rank_jitter(rank))
     if workload == "c1":
@@ -249,14 +258,28 @@ def main():
     import torch.distributed as dist
     from paper_2504_21627_b200 import lsnif, workloads as W
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    gloo = args.dist_backend == "gloo"
+    gpu = 0 if gloo else local_rank
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    coll_dev = torch.device("cpu") if gloo else dev
 
-    model = lsnif.GpuModel(MODEL_PATH, local_rank)
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    model = lsnif.GpuModel(MODEL_PATH, gpu)
     box = model.aabb
-    primary = build_rays(args.workload, rank, box)
+    strong = args.workload == "c5"
+    primary = build_rays(args.workload, rank, box, world)
     d_primary = lsnif.rays_to_tensor(primary, dev)
     d_hits_p = torch.empty((len(primary), 8), dtype=torch.int32, device=dev)
     mode_p = lsnif.CLOSEST
@@ -274,11 +297,15 @@ def main():
         model.query(d_shadow, lsnif.ANY, out=d_hits_s)
         stats_s = model.last_stats()
     n_step = len(primary) + len(shadow)
+    gathered = {}
 
     def step():
         model.query(d_primary, mode_p, out=d_hits_p)
         if d_shadow is not None:
             model.query(d_shadow, lsnif.ANY, out=d_hits_s)
+        if strong and world > 1:  # the one collective: result gather to rank 0
+            from paper_2504_21627_b200.dist import gather_to_rank0
+            gathered["hits"] = gather_to_rank0(d_hits_p if not gloo else d_hits_p.cpu())
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
@@ -305,12 +332,12 @@ def main():
     clocks.stop()
     model.profile_enable(False)
     prof = model.profile_read(reset=True)
-    elapsed_ms = sum(a.elapsed_time(b) for a, b in ev)
-    if world > 1:
-        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
-    value = world * n_step * args.steps / (elapsed_ms / 1e3)
+    elapsed_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
+    # weak scaling: every rank answers its own frame; strong (C5): one frame split
+    total_rays = n_step if strong and world == 1 else world * n_step
+    if strong:
+        total_rays = 3840 * 2160 * 16
+    value = total_rays * args.steps / (elapsed_ms / 1e3)
 
     # ---- e2e: same step through the host C-ABI entry (pinned buffers)
     pin_p = torch.from_numpy(primary.view(np.float32).reshape(-1, 8).copy()).pin_memory()
@@ -335,12 +362,8 @@ def main():
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_step()
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = world * n_step * e2e_steps / e2e_s
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e_value = total_rays * e2e_steps / e2e_s
     assert np.array_equal(hp.numpy(), d_hits_p.cpu().numpy()), "host/device results differ"
 
     if rank == 0:
@@ -375,12 +398,14 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None,
+            "scaling": "strong" if strong else "weak", "vs_baseline": None,
             "dtype": "f32 traversal/encode + f16xf16->f32 tcgen05 MLP", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.workload], "rays_per_step_per_gpu": n_step,
                        "primary_rays": len(primary), "shadow_rays": len(shadow),
                        "l2": "flushed between timed steps (256 MiB write outside the events)",
-                       "parallelism": f"dp{world} (one frame per GPU, no data-path collective)"},
+                       "parallelism": (f"dp{world} (row bands of one frame + NCCL result gather)"
+                                       if strong else
+                                       f"dp{world} (one frame per GPU, no data-path collective)")},
             "workload_stats": {
                 "frac_hit_aabb": (stats_p["pairs"] + stats_s["pairs"]) / n_step,
                 "frac_ge1_point": rows / n_step, "mean_points": pts / n_step,
