@@ -258,6 +258,27 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
   std::vector<uint32_t> occ((occ_bytes + 3) / 4, 0u);
   std::memcpy(occ.data(), d.occupancy, occ_bytes);
   m.occ = M.upload<uint32_t>(occ.data(), occ.size() * 4);
+  // padded stop mask: occupied cells + the border one cell outside the grid
+  {
+    const int Vp = V + 2;
+    const size_t nbits = static_cast<size_t>(Vp) * Vp * Vp;
+    std::vector<uint32_t> stop((nbits + 31) / 32, 0u);
+    for (int z = 0; z < Vp; ++z)
+      for (int y = 0; y < Vp; ++y)
+        for (int x = 0; x < Vp; ++x) {
+          const bool inside = x >= 1 && x <= V && y >= 1 && y <= V && z >= 1 && z <= V;
+          bool bit = true;
+          if (inside) {
+            const size_t i = static_cast<size_t>(x - 1) + static_cast<size_t>(V) *
+                             (static_cast<size_t>(y - 1) + static_cast<size_t>(V) * (z - 1));
+            bit = (d.occupancy[i >> 3] >> (i & 7)) & 1u;
+          }
+          const size_t j = static_cast<size_t>(x) + static_cast<size_t>(Vp) * (y + static_cast<size_t>(Vp) * z);
+          if (bit) stop[j >> 5] |= 1u << (j & 31);
+        }
+    m.stop = M.upload<uint32_t>(stop.data(), stop.size() * 4);
+    m.stop_words = static_cast<int>(stop.size());
+  }
 
   // hash tables: 4 binary16 per entry (8 B, one load per corner)
   float xmax = 0.0f;

@@ -35,6 +35,8 @@ struct DevModel {
   int M_pow2;
   int level_res[kMaxLevels];
   const uint32_t* occ;                 // V^3/32 words
+  const uint32_t* stop;                // (V+2)^3 bits: occupied cells + the outside border
+  int stop_words;
   const uint2* tables[kMaxLevels];     // M entries x 4 binary16 (F <= 4, zero padded)
   int hidden, n_out, n_mat, N3;        // N3: layer-3 MMA width (>= n_out, multiple of 16)
   const uint8_t* w_canon;              // W1 | W2 | W3, UMMA K-major canonical fp16
@@ -130,19 +132,19 @@ __device__ __forceinline__ bool slab_interval(const float o[3], const float d[3]
 }
 
 // State of one Amanatides-Woo walk (dda.cpp:40-117) in local unit-cube space.
-// The current cell is the linear occupancy index `idx` (x fastest,
-// voxel.hpp:30-34) plus, per axis, the number of cells left before the walk
-// leaves the grid; V is a power of two, so cell coordinates are bit fields
-// of idx. The entry plane of a stepped-into cell is derived from the new cell
-// when a point is emitted (dda.cpp:108: c_old+1 == c_new for +steps, c_old for
-// -steps) instead of being tracked every step.
+// The current cell is a linear index into the padded (V+2)^3 "stop" bitmask
+// (x fastest, voxel.hpp:30-34 order shifted by one), whose set bits are the
+// occupied cells plus the one-cell border outside the grid: a single SMEM
+// bit test per step finds both an occupied cell to emit and the walk leaving
+// the grid (dda.cpp:112), which is told apart only on that rare path. The
+// entry plane of a stepped-into cell is derived from the new cell when a point
+// is emitted (dda.cpp:108: c_old+1 == c_new for +steps, c_old for -steps).
 struct Walk {
   float o[3], d[3];    // nudged local origin and local direction
   float t1;
   float tn[3], td[3];  // t_next, t_delta
-  int rem[3];
-  int lin[3];          // linear-index increment of one step per axis
-  uint32_t idx;
+  int lin[3];          // padded linear-index increment of one step per axis
+  uint32_t idx;        // padded linear index of the current cell
   float t0;
   int axis0;           // entry axis of the start cell (-1: origin inside)
   float plane0;        // entry plane of the start cell (dda.cpp:86)
@@ -150,14 +152,18 @@ struct Walk {
 
 // dda.cpp:45-86 (+ renderer.cpp:252-253 world->local): nudge, clip, start
 // cell and stepping constants. Returns false when the local ray misses.
-__device__ __forceinline__ bool walk_setup(const DevModel& m, int log2v, const float wo[3],
-                                           const float wd[3], float t_min, Walk& w) {
+template <int VS>
+__device__ __forceinline__ bool walk_setup(const DevModel& m, const float wo[3], const float wd[3],
+                                           float t_min, Walk& w) {
+  const int V = VS ? VS : m.V;
+  const int Vp = V + 2;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     w.o[a] = __fmul_rn(__fsub_rn(wo[a], m.mn[a]), m.inv_ext[a]);
     w.d[a] = __fmul_rn(wd[a], m.inv_ext[a]);
   }
-  const float fres = m.fres;
+  const float fres = static_cast<float>(V);
+  const float inv_fres = m.inv_fres;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {  // dda.cpp:49-53
     const float scaled = __fmul_rn(w.o[a], fres);
@@ -170,33 +176,33 @@ __device__ __forceinline__ bool walk_setup(const DevModel& m, int log2v, const f
 #pragma unroll
   for (int a = 0; a < 3; ++a) start[a] = __fadd_rn(w.o[a], __fmul_rn(t0, w.d[a]));
   const float inf = __int_as_float(0x7f800000);
-  uint32_t idx = 0;
+  int c[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {  // dda.cpp:64-79
-    const int c = iclamp(static_cast<int>(floorf(__fmul_rn(start[a], fres))), 0, m.V - 1);
-    idx |= static_cast<uint32_t>(c) << (a * log2v);
+    c[a] = iclamp(static_cast<int>(floorf(__fmul_rn(start[a], fres))), 0, V - 1);
     const float da = w.d[a];
+    const int stride = a == 0 ? 1 : a == 1 ? Vp : Vp * Vp;
     if (da > 0.0f) {
       w.td[a] = __fdiv_rn(1.0f, __fmul_rn(fres, da));
       // (c + 1) / fres is exact as a product by 1/fres (fres a power of two)
-      w.tn[a] = __fadd_rn(t0, __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(c + 1), m.inv_fres),
+      w.tn[a] = __fadd_rn(t0, __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(c[a] + 1), inv_fres),
                                                   start[a]), da));
-      w.rem[a] = m.V - 1 - c;
-      w.lin[a] = 1 << (a * log2v);
+      w.lin[a] = stride;
     } else if (da < 0.0f) {
       w.td[a] = __fdiv_rn(-1.0f, __fmul_rn(fres, da));
-      w.tn[a] = __fadd_rn(t0, __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(c), m.inv_fres),
+      w.tn[a] = __fadd_rn(t0, __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(c[a]), inv_fres),
                                                   start[a]), da));
-      w.rem[a] = c;
-      w.lin[a] = -(1 << (a * log2v));
+      w.lin[a] = -stride;
     } else {
       w.td[a] = inf;
       w.tn[a] = inf;
-      w.rem[a] = 1 << 30;
       w.lin[a] = 0;
     }
   }
-  w.idx = idx;
+  // A zero direction would never leave its cell (the reference loops forever);
+  // such a walk stops after its start cell.
+  if (w.lin[0] == 0 && w.lin[1] == 0 && w.lin[2] == 0) w.t1 = -inf;
+  w.idx = static_cast<uint32_t>((c[0] + 1) + Vp * ((c[1] + 1) + Vp * (c[2] + 1)));
   w.t0 = t0;
   w.axis0 = entry_axis;
   w.plane0 = -1.0f;
@@ -207,35 +213,38 @@ __device__ __forceinline__ bool walk_setup(const DevModel& m, int log2v, const f
   return true;
 }
 
-__device__ __forceinline__ bool occ_bit(const uint32_t* occ, uint32_t idx) {
-  return (occ[idx >> 5] >> (idx & 31)) & 1u;
+__device__ __forceinline__ bool stop_bit(const uint32_t* stop, uint32_t idx) {
+  return (stop[idx >> 5] >> (idx & 31)) & 1u;
 }
 
-// One advance (dda.cpp:103-115): argmin of t_next with ties to the lower
-// axis, stop when it exceeds t1 or the cell leaves the grid. On success
-// `t` is the entry parameter of the new cell and `axis` its entry axis.
-__device__ __forceinline__ bool walk_advance(Walk& w, float& t, int& axis) {
-  const bool p1 = w.tn[1] < w.tn[0];
-  float tn = p1 ? w.tn[1] : w.tn[0];
-  const bool p2 = w.tn[2] < tn;
+// One advance (dda.cpp:103-115): argmin of t_next with ties to the lower axis
+// (p1: y beats x, p2: z beats the winner), stop when it exceeds t1; step the
+// winning axis. Returns false at the t1 exit; `tn` is the new entry t.
+__device__ __forceinline__ bool walk_step(Walk& w, float& tn, bool& p1, bool& p2) {
+  p1 = w.tn[1] < w.tn[0];
+  tn = p1 ? w.tn[1] : w.tn[0];
+  p2 = w.tn[2] < tn;
   tn = p2 ? w.tn[2] : tn;
   if (tn > w.t1) return false;
   const bool a0 = !p1 && !p2;
   const bool a1 = p1 && !p2;
-  if (a0) { w.tn[0] = __fadd_rn(w.tn[0], w.td[0]); w.rem[0] -= 1; w.idx += w.lin[0]; }
-  if (a1) { w.tn[1] = __fadd_rn(w.tn[1], w.td[1]); w.rem[1] -= 1; w.idx += w.lin[1]; }
-  if (p2) { w.tn[2] = __fadd_rn(w.tn[2], w.td[2]); w.rem[2] -= 1; w.idx += w.lin[2]; }
-  if ((w.rem[0] | w.rem[1] | w.rem[2]) < 0) return false;
-  t = tn;
-  axis = p2 ? 2 : (p1 ? 1 : 0);
+  if (a0) w.tn[0] = __fadd_rn(w.tn[0], w.td[0]);
+  if (a1) w.tn[1] = __fadd_rn(w.tn[1], w.td[1]);
+  if (p2) w.tn[2] = __fadd_rn(w.tn[2], w.td[2]);
+  int dl = p1 ? w.lin[1] : w.lin[0];
+  dl = p2 ? w.lin[2] : dl;
+  w.idx += static_cast<uint32_t>(dl);
   return true;
 }
 
-// Entry plane (in grid units) of the cell `idx` entered along `axis`.
-__device__ __forceinline__ float walk_plane(const Walk& w, int log2v, int V, int axis) {
-  const int c = static_cast<int>(w.idx >> (axis * log2v)) & (V - 1);
-  const float da = axis == 0 ? w.d[0] : axis == 1 ? w.d[1] : w.d[2];
-  return static_cast<float>(da > 0.0f ? c : c + 1);
+// Cell coordinates (unpadded, may be -1 or V when outside) of a padded index.
+template <int VS>
+__device__ __forceinline__ void walk_cell(const DevModel& m, uint32_t idx, int c[3]) {
+  const uint32_t Vp = static_cast<uint32_t>((VS ? VS : m.V) + 2);
+  const uint32_t q = idx / Vp;
+  c[0] = static_cast<int>(idx - q * Vp) - 1;
+  c[1] = static_cast<int>(q % Vp) - 1;
+  c[2] = static_cast<int>(q / Vp) - 1;
 }
 
 // Pool entry of one boundary point: entry t and (axis | plane << 2), axis 3
@@ -293,10 +302,11 @@ __device__ __forceinline__ int plane_axis_of(const float p[3], float fv) {
 // in-plane corners. With the plane axis a and free axes b < c, the
 // reference's corner order (dx,dy,dz bits, skipping the +1 side of a) is
 // (db,dc) = (0,0),(1,0),(0,1),(1,1) and its weight wx*wy*wz = wb*wc exactly
-// (the plane factor is 1 - 0). F <= 4 features, fp32 accumulation.
+// (the plane factor is 1 - 0). Split into index/weight computation and the
+// fp32 accumulation so callers can issue every gather of a point first.
 template <bool POW2>
-__device__ __forceinline__ void encode_boundary_level(const DevModel& m, int level, const float p[3],
-                                                      int pa, float feat[4], uint32_t* hidx) {
+__device__ __forceinline__ void boundary_corners(const DevModel& m, int level, const float p[3], int pa,
+                                                 uint32_t idx[4], float w[4]) {
   const int res = m.level_res[level];
   const float fres = static_cast<float>(res);
   const int b = pa == 0 ? 1 : 0;
@@ -316,21 +326,19 @@ __device__ __forceinline__ void encode_boundary_level(const DevModel& m, int lev
   const uint32_t ha = static_cast<uint32_t>(base_a) * Pa;
   const uint32_t hb0 = static_cast<uint32_t>(base_b) * Pb, hb1 = hb0 + Pb;
   const uint32_t hc0 = static_cast<uint32_t>(base_c) * Pc, hc1 = hc0 + Pc;
-  uint32_t idx[4];
   idx[0] = hash_reduce<POW2>(m, ha ^ hb0 ^ hc0);
   idx[1] = hash_reduce<POW2>(m, ha ^ hb1 ^ hc0);
   idx[2] = hash_reduce<POW2>(m, ha ^ hb0 ^ hc1);
   idx[3] = hash_reduce<POW2>(m, ha ^ hb1 ^ hc1);
-  const uint2* table = m.tables[level];
-  uint2 ent[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) ent[k] = __ldg(table + idx[k]);
-  if (hidx) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) hidx[k] = idx[k];
-  }
   const float wb0 = __fsub_rn(1.0f, fb), wc0 = __fsub_rn(1.0f, fc);
-  const float w[4] = {__fmul_rn(wb0, wc0), __fmul_rn(fb, wc0), __fmul_rn(wb0, fc), __fmul_rn(fb, fc)};
+  w[0] = __fmul_rn(wb0, wc0);
+  w[1] = __fmul_rn(fb, wc0);
+  w[2] = __fmul_rn(wb0, fc);
+  w[3] = __fmul_rn(fb, fc);
+}
+
+// features[f] = sum_k w[k] * entry_k[f] in corner order, fp32, unfused.
+__device__ __forceinline__ void accumulate4(const uint2 ent[4], const float w[4], float feat[4]) {
   feat[0] = feat[1] = feat[2] = feat[3] = 0.0f;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
@@ -339,6 +347,23 @@ __device__ __forceinline__ void encode_boundary_level(const DevModel& m, int lev
 #pragma unroll
     for (int f = 0; f < 4; ++f) feat[f] = __fadd_rn(feat[f], __fmul_rn(w[k], t[f]));
   }
+}
+
+template <bool POW2>
+__device__ __forceinline__ void encode_boundary_level(const DevModel& m, int level, const float p[3],
+                                                      int pa, float feat[4], uint32_t* hidx) {
+  uint32_t idx[4];
+  float w[4];
+  boundary_corners<POW2>(m, level, p, pa, idx, w);
+  const uint2* table = m.tables[level];
+  uint2 ent[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) ent[k] = __ldg(table + idx[k]);
+  if (hidx) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) hidx[k] = idx[k];
+  }
+  accumulate4(ent, w, feat);
 }
 
 // Volume fallback (first point of a ray starting inside an occupied cell):

@@ -27,7 +27,7 @@ namespace lsnif_dev {
 // 128-ray batches. Per warp: DDA per lane (points -> 8-byte pool entries),
 // then a warp-cooperative encode of all pooled points. LS/FS: compile-time
 // level/feature counts (0 = read from the model); POW2: M is a power of two.
-template <bool DEBUG, int LS, int FS, bool POW2>
+template <bool DEBUG, int LS, int FS, bool POW2, int VS>
 __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   const DevModel& m = P.m;
@@ -35,28 +35,42 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
   const int F = FS ? FS : m.F;
   const int LF = L * F;
   const int H = m.H;
-  const int V = m.V;
-  const int log2v = __ffs(V) - 1;
-  const int occ_words = (V * V * V) >> 5;
-  for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.occ + i);
+  const int V = VS ? VS : m.V;
+  const int occ_words = m.stop_words;
+  for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.stop + i);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint2* pool = reinterpret_cast<uint2*>(smem + ((occ_words + 3) & ~3)) + warp * (H * 32);
   __syncthreads();
   const float scale = m.act_scale;
   const int64_t nbatch = (P.n + 127) / 128;
+  uint32_t st_pair = 0, st_rows = 0, st_pts = 0, st_vol = 0;  // query statistics
 
+  // software-pipelined ray loads: the next batch's ray is in flight while
+  // the current one is traversed
+  float4 nra = make_float4(0, 0, 0, 0), nrb = nra;
+  {
+    const int64_t first = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
+    if (first < P.n) {
+      const float4* r4 = reinterpret_cast<const float4*>(P.rays + first);
+      nra = __ldg(r4);
+      nrb = __ldg(r4 + 1);
+    }
+  }
   for (int64_t batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
     const int64_t ray_idx = batch * 128 + threadIdx.x;
     const bool live = ray_idx < P.n;
-    float o[3] = {0, 0, 0}, d[3] = {0, 0, 0}, t_min = 0.0f, t_max = 0.0f;
-    if (live) {
-      const float4* r4 = reinterpret_cast<const float4*>(P.rays + ray_idx);
-      const float4 ra = __ldg(r4), rb = __ldg(r4 + 1);
-      o[0] = ra.x; o[1] = ra.y; o[2] = ra.z;
-      d[0] = ra.w; d[1] = rb.x; d[2] = rb.y;
-      t_min = rb.z; t_max = rb.w;
+    const float4 ra = nra, rb = nrb;
+    {
+      const int64_t nxt = ray_idx + static_cast<int64_t>(gridDim.x) * 128;
+      if (nxt < P.n) {
+        const float4* r4 = reinterpret_cast<const float4*>(P.rays + nxt);
+        nra = __ldg(r4);
+        nrb = __ldg(r4 + 1);
+      }
     }
+    float o[3] = {ra.x, ra.y, ra.z}, d[3] = {ra.w, rb.x, rb.y};
+    const float t_min = rb.z, t_max = rb.w;
     float enter = 0.0f, exit = 0.0f;
     const bool pair = live && frame_interval(m, o, d, t_min, t_max, enter, exit);
 
@@ -64,23 +78,32 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
     Walk w;
     int count = 0;
     bool fio = false;
-    if (pair && walk_setup(m, log2v, o, d, t_min, w)) {
-      if (occ_bit(smem, w.idx)) {
+    if (pair && walk_setup<VS>(m, o, d, t_min, w)) {
+      if (stop_bit(smem, w.idx)) {  // start cell (always inside the grid)
         fio = w.axis0 < 0;
         pool[lane] = pack_point(w.t0, w.axis0, w.plane0);
-        if (DEBUG) P.cells[ray_idx * H] = (w.idx & (V - 1)) | ((w.idx >> log2v) & (V - 1)) << 8 |
-                                          ((w.idx >> (2 * log2v)) & (V - 1)) << 16;
+        if (DEBUG) {
+          int c[3];
+          walk_cell<VS>(m, w.idx, c);
+          P.cells[ray_idx * H] = c[0] | c[1] << 8 | c[2] << 16;
+        }
         count = 1;
       }
-      float t;
-      int axis;
-      while (count < H && walk_advance(w, t, axis)) {
-        if (occ_bit(smem, w.idx)) {
-          pool[count * 32 + lane] = pack_point(t, axis, walk_plane(w, log2v, V, axis));
-          if (DEBUG)
-            P.cells[ray_idx * H + count] = (w.idx & (V - 1)) | ((w.idx >> log2v) & (V - 1)) << 8 |
-                                           ((w.idx >> (2 * log2v)) & (V - 1)) << 16;
-          ++count;
+      float tn;
+      bool p1, p2;
+      if (count < H) {
+        while (walk_step(w, tn, p1, p2)) {
+          if (stop_bit(smem, w.idx)) {
+            int c[3];
+            walk_cell<VS>(m, w.idx, c);
+            const int axis = p2 ? 2 : (p1 ? 1 : 0);
+            const int ca = axis == 0 ? c[0] : axis == 1 ? c[1] : c[2];
+            if (ca < 0 || ca >= V) break;  // left the grid (dda.cpp:112)
+            const float da = axis == 0 ? w.d[0] : axis == 1 ? w.d[1] : w.d[2];
+            pool[count * 32 + lane] = pack_point(tn, axis, static_cast<float>(da > 0.0f ? ca : ca + 1));
+            if (DEBUG) P.cells[ray_idx * H + count] = c[0] | c[1] << 8 | c[2] << 16;
+            if (++count >= H) break;  // first-H truncation (dda.cpp:99)
+          }
         }
       }
     }
@@ -115,15 +138,10 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
         dst[0] = make_float4(__int_as_float(static_cast<int32_t>(ray_idx)), enter, exit, t_min);
         dst[1] = make_float4(t_max, 0.0f, 0.0f, 0.0f);
       }
-      const int n_pair = __popc(__ballot_sync(0xffffffffu, pair));
-      const int n_pts = __reduce_add_sync(0xffffffffu, valid ? count : 0);
-      const int n_vol = __popc(__ballot_sync(0xffffffffu, valid && fio));
-      if (lane == 0 && n_pair) {
-        atomicAdd(P.stats + 0, static_cast<unsigned long long>(n_pair));
-        atomicAdd(P.stats + 1, static_cast<unsigned long long>(__popc(vmask)));
-        atomicAdd(P.stats + 2, static_cast<unsigned long long>(n_pts));
-        atomicAdd(P.stats + 3, static_cast<unsigned long long>(n_vol));
-      }
+      st_pair += pair ? 1u : 0u;
+      st_rows += valid ? 1u : 0u;
+      st_pts += valid ? static_cast<uint32_t>(count) : 0u;
+      st_vol += (valid && fio) ? 1u : 0u;
     }
 
     // ---- warp-cooperative encode of all pooled points (encoding.hpp:166-176)
@@ -161,24 +179,58 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
       unpack_point(e, ro, rd, m.inv_fres, p, volume);
       float fv[16];
       const int pa = volume ? -1 : plane_axis_of(p, m.fres);
+      if (LS == 2 && !volume) {
+        // both levels' 8 gathers in flight before any accumulation
+        uint32_t i0[4], i1[4];
+        float w0[4], w1[4];
+        boundary_corners<POW2>(m, 0, p, pa, i0, w0);
+        boundary_corners<POW2>(m, 1, p, pa, i1, w1);
+        uint2 e0[4], e1[4];
 #pragma unroll
-      for (int l = 0; l < (LS ? LS : kMaxLevels); ++l) {
-        if (!LS && l >= L) break;
-        float feat[4];
-        uint32_t hidx[8];
-        if (volume)
-          encode_volume_level<POW2>(m, l, p, feat, DEBUG ? hidx : nullptr);
-        else
-          encode_boundary_level<POW2>(m, l, p, pa, feat, DEBUG ? hidx : nullptr);
-        if (DEBUG) {
-          const int64_t hb = ((o_ray * H + k) * L + l) * 8;
-          const int nc = volume ? 8 : 4;
-          for (int q = 0; q < nc; ++q) P.hidx[hb + q] = hidx[q];
-          for (int f = 0; f < F; ++f) P.feat[o_ray * m.K1 + k * LF + l * F + f] = feat[f];
+        for (int q = 0; q < 4; ++q) {
+          e0[q] = __ldg(m.tables[0] + i0[q]);
+          e1[q] = __ldg(m.tables[1] + i1[q]);
         }
+        float f0[4], f1[4];
+        accumulate4(e0, w0, f0);
+        accumulate4(e1, w1, f1);
 #pragma unroll
         for (int f = 0; f < 4; ++f)
-          if (f < F) fv[l * F + f] = feat[f];
+          if (f < F) {
+            fv[f] = f0[f];
+            fv[F + f] = f1[f];
+          }
+        if (DEBUG) {
+          const int64_t hb = (o_ray * H + k) * L * 8;
+          for (int q = 0; q < 4; ++q) {
+            P.hidx[hb + q] = i0[q];
+            P.hidx[hb + 8 + q] = i1[q];
+          }
+          for (int f = 0; f < F; ++f) {
+            P.feat[o_ray * m.K1 + k * LF + f] = f0[f];
+            P.feat[o_ray * m.K1 + k * LF + F + f] = f1[f];
+          }
+        }
+      } else {
+#pragma unroll
+        for (int l = 0; l < (LS ? LS : kMaxLevels); ++l) {
+          if (!LS && l >= L) break;
+          float feat[4];
+          uint32_t hidx[8];
+          if (volume)
+            encode_volume_level<POW2>(m, l, p, feat, DEBUG ? hidx : nullptr);
+          else
+            encode_boundary_level<POW2>(m, l, p, pa, feat, DEBUG ? hidx : nullptr);
+          if (DEBUG) {
+            const int64_t hb = ((o_ray * H + k) * L + l) * 8;
+            const int nc = volume ? 8 : 4;
+            for (int q = 0; q < nc; ++q) P.hidx[hb + q] = hidx[q];
+            for (int f = 0; f < F; ++f) P.feat[o_ray * m.K1 + k * LF + l * F + f] = feat[f];
+          }
+#pragma unroll
+          for (int f = 0; f < 4; ++f)
+            if (f < F) fv[l * F + f] = feat[f];
+        }
       }
       if (DEBUG) {
         P.t[o_ray * H + k] = __uint_as_float(e.x);
@@ -224,6 +276,18 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
       }
     }
     __syncwarp();  // pool reuse by the next batch
+  }
+  if (!DEBUG) {  // one set of statistics atomics per warp
+    const uint32_t a = __reduce_add_sync(0xffffffffu, st_pair);
+    const uint32_t b = __reduce_add_sync(0xffffffffu, st_rows);
+    const uint32_t c = __reduce_add_sync(0xffffffffu, st_pts);
+    const uint32_t e = __reduce_add_sync(0xffffffffu, st_vol);
+    if (lane == 0 && a) {
+      atomicAdd(P.stats + 0, static_cast<unsigned long long>(a));
+      atomicAdd(P.stats + 1, static_cast<unsigned long long>(b));
+      atomicAdd(P.stats + 2, static_cast<unsigned long long>(c));
+      atomicAdd(P.stats + 3, static_cast<unsigned long long>(e));
+    }
   }
 }
 
@@ -490,7 +554,7 @@ __global__ void __launch_bounds__(128) infer_f32_kernel(const DevModel m, const 
 // ================================================================ launch
 
 size_t trace_smem_bytes(const DevModel& m) {
-  const size_t occ_words = (static_cast<size_t>(m.V) * m.V * m.V) >> 5;
+  const size_t occ_words = static_cast<size_t>(m.stop_words);
   return ((occ_words + 3) & ~size_t(3)) * 4 + 4 * static_cast<size_t>(m.H) * 32 * 8;
 }
 
@@ -500,9 +564,9 @@ size_t mlp_smem_bytes(const DevModel& m) {
   return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + 2 * x + 2 * h + 128;
 }
 
-template <bool DEBUG, int LS, int FS, bool POW2>
+template <bool DEBUG, int LS, int FS, bool POW2, int VS>
 static cudaError_t launch_trace_t(const TraceParams& p, cudaStream_t st) {
-  auto kern = trace_encode_kernel<DEBUG, LS, FS, POW2>;
+  auto kern = trace_encode_kernel<DEBUG, LS, FS, POW2, VS>;
   const size_t smem = trace_smem_bytes(p.m);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
@@ -519,9 +583,10 @@ static cudaError_t launch_trace_t(const TraceParams& p, cudaStream_t st) {
 
 cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st) {
   if (p.n <= 0) return cudaSuccess;
-  const bool fast = p.m.L == 2 && p.m.F == 3 && p.m.M_pow2;
-  if (debug) return fast ? launch_trace_t<true, 2, 3, true>(p, st) : launch_trace_t<true, 0, 0, false>(p, st);
-  return fast ? launch_trace_t<false, 2, 3, true>(p, st) : launch_trace_t<false, 0, 0, false>(p, st);
+  const bool fast = p.m.L == 2 && p.m.F == 3 && p.m.M_pow2 && p.m.V == 32;
+  if (debug)
+    return fast ? launch_trace_t<true, 2, 3, true, 32>(p, st) : launch_trace_t<true, 0, 0, false, 0>(p, st);
+  return fast ? launch_trace_t<false, 2, 3, true, 32>(p, st) : launch_trace_t<false, 0, 0, false, 0>(p, st);
 }
 
 cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st) {
