@@ -138,7 +138,9 @@ struct HostStaging {
 constexpr int64_t kChunk = int64_t(1) << 21;      // rays per trace/MLP launch pair
 constexpr int64_t kHostChunk = int64_t(1) << 20;  // rays per host staging step
 constexpr size_t kMaxChunks = 1024;                // row counters per query (2^31 rays)
-constexpr size_t kCounterBytes = 32 + 4 * kMaxChunks;
+// counter block, zeroed by one memset per query: 4 x u64 stats | u32 row
+// counter per chunk | u64 batch counter per chunk
+constexpr size_t kCounterBytes = 32 + 4 * kMaxChunks + 8 * kMaxChunks;
 
 }  // namespace
 
@@ -537,7 +539,7 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
   ck(cudaSetDevice(M.device), "cudaSetDevice");
   Workspace& w = M.workspace(st, std::max<int64_t>(n, 1));
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
-  ck(cudaMemsetAsync(w.stats, 0, 32 + 4 * static_cast<size_t>(nchunks), st), "cudaMemsetAsync");
+  ck(cudaMemsetAsync(w.stats, 0, kCounterBytes, st), "cudaMemsetAsync");
   w.last_rays = n;
   for (int64_t s = 0, ci = 0; s < n; s += kChunk, ++ci) {
     const int64_t cn = std::min(kChunk, n - s);
@@ -550,6 +552,7 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     tp.X = w.X;
     tp.meta = w.meta;
     tp.row_counter = w.counter + ci;
+    tp.batch_counter = reinterpret_cast<unsigned long long*>(w.counter + kMaxChunks) + ci;
     tp.stats = w.stats;
     tp.tile_bytes = M.tile_bytes();
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -707,10 +710,15 @@ lsnif_status lsnif_debug_traverse(lsnif_model model, const lsnif_ray* d_rays, in
     ck(cudaMemsetAsync(cells, 0xff, n * H * 4, st), "memset");
     ck(cudaMemsetAsync(hidx, 0xff, n * H * L * 8 * 4, st), "memset");
     ck(cudaMemsetAsync(feat, 0, n * static_cast<size_t>(m.K1) * 4, st), "memset");
+    Workspace& w = model->workspace(st, 1);
+    ck(cudaMemsetAsync(w.stats, 0, kCounterBytes, st), "cudaMemsetAsync");
     lsnif_dev::TraceParams tp{};
     tp.m = m;
     tp.rays = d_rays;
     tp.n = n;
+    tp.row_counter = w.counter;
+    tp.batch_counter = reinterpret_cast<unsigned long long*>(w.counter + kMaxChunks);
+    tp.stats = w.stats;
     tp.info = info;
     tp.interval = interval;
     tp.t = t;

@@ -82,7 +82,7 @@ __device__ __forceinline__ bool frame_interval(const DevModel& m, const float o[
       if (o[a] < m.mn[a] || o[a] > m.mx[a]) return false;
       continue;
     }
-    const float inv = __fdiv_rn(1.0f, d[a]);
+    const float inv = __frcp_rn(d[a]);  // == 1.0f / d (correctly rounded)
     float ta = __fmul_rn(__fsub_rn(m.mn[a], o[a]), inv);
     float tb = __fmul_rn(__fsub_rn(m.mx[a], o[a]), inv);
     if (ta > tb) {
@@ -113,7 +113,7 @@ __device__ __forceinline__ bool slab_interval(const float o[3], const float d[3]
       if (o[a] < 0.0f || o[a] > 1.0f) return false;
       continue;
     }
-    const float inv = __fdiv_rn(1.0f, d[a]);
+    const float inv = __frcp_rn(d[a]);  // == 1.0f / d (correctly rounded)
     float ta = __fmul_rn(__fsub_rn(0.0f, o[a]), inv);
     float tb = __fmul_rn(__fsub_rn(1.0f, o[a]), inv);
     if (ta > tb) {
@@ -183,13 +183,13 @@ __device__ __forceinline__ bool walk_setup(const DevModel& m, const float wo[3],
     const float da = w.d[a];
     const int stride = a == 0 ? 1 : a == 1 ? Vp : Vp * Vp;
     if (da > 0.0f) {
-      w.td[a] = __fdiv_rn(1.0f, __fmul_rn(fres, da));
+      w.td[a] = __frcp_rn(__fmul_rn(fres, da));
       // (c + 1) / fres is exact as a product by 1/fres (fres a power of two)
       w.tn[a] = __fadd_rn(t0, __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(c[a] + 1), inv_fres),
                                                   start[a]), da));
       w.lin[a] = stride;
     } else if (da < 0.0f) {
-      w.td[a] = __fdiv_rn(-1.0f, __fmul_rn(fres, da));
+      w.td[a] = -__frcp_rn(__fmul_rn(fres, da));  // == -1 / (fres*da) exactly
       w.tn[a] = __fadd_rn(t0, __fdiv_rn(__fsub_rn(__fmul_rn(static_cast<float>(c[a]), inv_fres),
                                                   start[a]), da));
       w.lin[a] = -stride;

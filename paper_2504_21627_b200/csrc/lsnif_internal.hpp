@@ -19,6 +19,7 @@ struct TraceParams {
   uint8_t* X;                 // compacted MLP operand tiles
   RowMeta* meta;
   int32_t* row_counter;
+  unsigned long long* batch_counter;  // dynamic 32-ray batch claims (zeroed per launch)
   unsigned long long* stats;  // pairs, rows, points, volume points
   uint32_t tile_bytes;
   // debug probe (DEBUG=true only)

@@ -41,34 +41,40 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   uint2* pool = reinterpret_cast<uint2*>(smem + ((occ_words + 3) & ~3)) + warp * (H * 32);
+  // per-lane local ray (o, d) + MLP row, read by the encoding lanes
+  float4* lane_ray = reinterpret_cast<float4*>(smem + ((occ_words + 3) & ~3) + 4 * 2 * H * 32) + warp * 64;
   __syncthreads();
   const float scale = m.act_scale;
   const int64_t nbatch = (P.n + 127) / 128;
   uint32_t st_pair = 0, st_rows = 0, st_pts = 0, st_vol = 0;  // query statistics
+  const int64_t nwb = (P.n + 31) / 32;  // 32-ray warp batches, fetched dynamically
 
-  // software-pipelined ray loads: the next batch's ray is in flight while
-  // the current one is traversed
+  // Each warp claims 32-ray batches from a global counter; the next claim
+  // and the next batch's ray loads are issued before the current batch is
+  // traversed (software pipelining), so warps never wait on each other.
+  auto claim = [&]() -> int64_t {
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(P.batch_counter, 1ull);
+    return static_cast<int64_t>(__shfl_sync(0xffffffffu, b, 0));
+  };
   float4 nra = make_float4(0, 0, 0, 0), nrb = nra;
-  {
-    const int64_t first = static_cast<int64_t>(blockIdx.x) * 128 + threadIdx.x;
-    if (first < P.n) {
-      const float4* r4 = reinterpret_cast<const float4*>(P.rays + first);
+  auto load_ray = [&](int64_t wb) {
+    const int64_t r = wb * 32 + lane;
+    if (wb < nwb && r < P.n) {
+      const float4* r4 = reinterpret_cast<const float4*>(P.rays + r);
       nra = __ldg(r4);
       nrb = __ldg(r4 + 1);
     }
-  }
-  for (int64_t batch = blockIdx.x; batch < nbatch; batch += gridDim.x) {
-    const int64_t ray_idx = batch * 128 + threadIdx.x;
+  };
+  int64_t next_wb = claim();
+  load_ray(next_wb);
+  while (next_wb < nwb) {
+    const int64_t wbatch = next_wb;
+    const int64_t ray_idx = wbatch * 32 + lane;
     const bool live = ray_idx < P.n;
     const float4 ra = nra, rb = nrb;
-    {
-      const int64_t nxt = ray_idx + static_cast<int64_t>(gridDim.x) * 128;
-      if (nxt < P.n) {
-        const float4* r4 = reinterpret_cast<const float4*>(P.rays + nxt);
-        nra = __ldg(r4);
-        nrb = __ldg(r4 + 1);
-      }
-    }
+    next_wb = claim();
+    load_ray(next_wb);
     float o[3] = {ra.x, ra.y, ra.z}, d[3] = {ra.w, rb.x, rb.y};
     const float t_min = rb.z, t_max = rb.w;
     float enter = 0.0f, exit = 0.0f;
@@ -144,6 +150,11 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
       st_vol += (valid && fio) ? 1u : 0u;
     }
 
+    if (valid) {
+      lane_ray[2 * lane] = make_float4(w.o[0], w.o[1], w.o[2], __int_as_float(row));
+      lane_ray[2 * lane + 1] = make_float4(w.d[0], w.d[1], w.d[2], 0.0f);
+    }
+    __syncwarp();
     // ---- warp-cooperative encode of all pooled points (encoding.hpp:166-176)
     const int c = valid ? count : 0;
     int incl = c;
@@ -163,15 +174,11 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
         if (ex <= j) owner += st;
       }
       const int o_excl = __shfl_sync(0xffffffffu, excl, owner);
-      const int o_row = __shfl_sync(0xffffffffu, row, owner);
-      float ro[3], rd[3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        ro[a] = __shfl_sync(0xffffffffu, w.o[a], owner);
-        rd[a] = __shfl_sync(0xffffffffu, w.d[a], owner);
-      }
-      const int64_t o_ray = batch * 128 + warp * 32 + owner;
+      const int64_t o_ray = wbatch * 32 + owner;
       if (j >= total) continue;
+      const float4 rq = lane_ray[2 * owner], rr = lane_ray[2 * owner + 1];
+      const float ro[3] = {rq.x, rq.y, rq.z}, rd[3] = {rr.x, rr.y, rr.z};
+      const int o_row = __float_as_int(rq.w);
       const int k = j - o_excl;
       const uint2 e = pool[k * 32 + owner];
       float p[3];
@@ -555,7 +562,7 @@ __global__ void __launch_bounds__(128) infer_f32_kernel(const DevModel m, const 
 
 size_t trace_smem_bytes(const DevModel& m) {
   const size_t occ_words = static_cast<size_t>(m.stop_words);
-  return ((occ_words + 3) & ~size_t(3)) * 4 + 4 * static_cast<size_t>(m.H) * 32 * 8;
+  return ((occ_words + 3) & ~size_t(3)) * 4 + 4 * static_cast<size_t>(m.H) * 32 * 8 + 4 * 64 * 16;
 }
 
 size_t mlp_smem_bytes(const DevModel& m) {
