@@ -166,6 +166,46 @@ lsnif_status lsnif_debug_traverse(lsnif_model model, const lsnif_ray* d_rays, in
 /* Counters of the most recent lsnif_query on `stream` (synchronises it). */
 lsnif_status lsnif_last_query_stats(lsnif_model model, void* stream, lsnif_query_stats* out);
 
+/* ---- multi-object scenes ----
+ * An instance places a model in the world: world_to_object is the 3x4
+ * row-major affine [linear | translation] the reference stores as
+ * PreparedObject::world_to_object (renderer.hpp:67-71). Models may be shared
+ * by several instances (renderer.cpp:55-76). */
+typedef struct lsnif_instance {
+  lsnif_model model;
+  float world_to_object[12];
+} lsnif_instance;
+
+/* lsnif::SurfaceHit (renderer.hpp:56-65) for the merged multi-object query,
+ * 64 B. object_index = -1 when no instance was accepted. In ANY mode only
+ * flags / object_index (the first instance that occludes) are set. */
+typedef struct lsnif_scene_hit {
+  float t;
+  float position[3];
+  float normal[3];  /* unit, world space, facing the incoming ray */
+  float albedo[3];
+  uint32_t kind;    /* MaterialKind of the model's material table */
+  float roughness;
+  int32_t object_index;
+  uint32_t flags;   /* 1: hit (CLOSEST) / occluded (ANY) */
+  uint32_t pad[2];
+} lsnif_scene_hit;
+
+typedef struct lsnif_scene_s* lsnif_scene;
+
+/* Replaces the LSNIF part of PreparedScene::prepare (renderer.cpp:83-97):
+ * the instance list; the models must live on one device and outlive the scene. */
+lsnif_status lsnif_scene_create(const lsnif_instance* instances, int32_t n, lsnif_scene* out);
+lsnif_status lsnif_scene_destroy(lsnif_scene scene);
+/* Replaces the LSNIF phases of intersect_scene (mode CLOSEST,
+ * renderer.cpp:277-303) and occluded_batch (mode ANY, 310-323) for a scene
+ * without triangle objects: broad phase (collect_pairs, 154-181, exact
+ * per-instance frame-box test instead of the top-level BVH prefilter),
+ * per-object narrow phase in object order, and the accept/merge rules.
+ * WORLD-space DEVICE rays in, one lsnif_scene_hit per ray out. */
+lsnif_status lsnif_scene_query(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n, int mode,
+                               lsnif_scene_hit* d_hits, void* stream);
+
 /* Kernel-level timing of queries (bench / roofline support). When enabled,
  * CUDA events are recorded on the query stream around every kernel launch;
  * lsnif_profile_read synchronises `stream` and returns the summed device

@@ -828,4 +828,201 @@ void narrow_phase(const Model& m, const Ray* rays, int64_t n, int mode, HitRecor
   for (auto& t : pool) t.join();
 }
 
+// ------------------------------------------------------ procedural meshes
+
+static void mesh_finalize(ObjMesh& m) {  // shapes.cpp:10-14
+  m.face_material.assign(m.faces.size() / 3, 0);
+  m.n_mat = 1;
+}
+
+// shapes.cpp:18-58
+ObjMesh make_uv_sphere(float radius, int segments, int rings) {
+  const float kPi = 3.14159265358979323846f;
+  ObjMesh m;
+  auto push = [&](float x, float y, float z) { m.verts.insert(m.verts.end(), {x, y, z}); };
+  push(0, radius, 0);
+  for (int r = 1; r < rings; ++r) {
+    const float phi = kPi * static_cast<float>(r) / static_cast<float>(rings);
+    for (int s = 0; s < segments; ++s) {
+      const float theta = 2.0f * kPi * static_cast<float>(s) / static_cast<float>(segments);
+      push(radius * (std::sin(phi) * std::cos(theta)), radius * std::cos(phi),
+           radius * (std::sin(phi) * std::sin(theta)));
+    }
+  }
+  push(0, -radius, 0);
+  const int south = static_cast<int>(m.verts.size() / 3) - 1;
+  auto rv = [&](int r, int s) { return 1 + (r - 1) * segments + (s % segments); };
+  auto face = [&](int a, int b, int c) { m.faces.insert(m.faces.end(), {a, b, c}); };
+  for (int s = 0; s < segments; ++s) face(0, rv(1, s + 1), rv(1, s));
+  for (int r = 1; r < rings - 1; ++r)
+    for (int s = 0; s < segments; ++s) {
+      const int a = rv(r, s), b = rv(r, s + 1), c = rv(r + 1, s), d = rv(r + 1, s + 1);
+      face(a, b, d);
+      face(a, d, c);
+    }
+  for (int s = 0; s < segments; ++s) face(south, rv(rings - 1, s), rv(rings - 1, s + 1));
+  mesh_finalize(m);
+  return m;
+}
+
+// shapes.cpp:60-87
+ObjMesh make_box(const float h[3]) {
+  ObjMesh m;
+  const int axes[6][2] = {{1, 2}, {2, 0}, {0, 1}, {2, 1}, {0, 2}, {1, 0}};
+  for (int face = 0; face < 6; ++face) {
+    const int axis = face % 3;
+    const float sign = face < 3 ? 1.0f : -1.0f;
+    float n[3] = {0, 0, 0}, u[3] = {0, 0, 0}, v[3] = {0, 0, 0}, c[3];
+    n[axis] = sign;
+    u[axes[face][0]] = h[axes[face][0]];
+    v[axes[face][1]] = h[axes[face][1]];
+    for (int k = 0; k < 3; ++k) c[k] = n[k] * h[k];
+    const int base = static_cast<int>(m.verts.size() / 3);
+    for (int k = 0; k < 3; ++k) m.verts.push_back(c[k] - u[k] - v[k]);
+    for (int k = 0; k < 3; ++k) m.verts.push_back(c[k] + u[k] - v[k]);
+    for (int k = 0; k < 3; ++k) m.verts.push_back(c[k] + u[k] + v[k]);
+    for (int k = 0; k < 3; ++k) m.verts.push_back(c[k] - u[k] + v[k]);
+    m.faces.insert(m.faces.end(), {base, base + 1, base + 2, base, base + 2, base + 3});
+  }
+  mesh_finalize(m);
+  return m;
+}
+
+// shapes.cpp:89-112
+ObjMesh make_torus(float R, float r0, int segments, int rings) {
+  const float kPi = 3.14159265358979323846f;
+  ObjMesh m;
+  for (int s = 0; s < segments; ++s) {
+    const float theta = 2.0f * kPi * static_cast<float>(s) / static_cast<float>(segments);
+    const float cx = R * std::cos(theta), cz = R * std::sin(theta);
+    const float rx = std::cos(theta), rz = std::sin(theta);
+    for (int r = 0; r < rings; ++r) {
+      const float phi = 2.0f * kPi * static_cast<float>(r) / static_cast<float>(rings);
+      const float nx = std::cos(phi) * rx, ny = std::sin(phi), nz = std::cos(phi) * rz;
+      m.verts.insert(m.verts.end(), {cx + r0 * nx, r0 * ny, cz + r0 * nz});
+    }
+  }
+  auto vid = [&](int s, int r) { return (s % segments) * rings + (r % rings); };
+  for (int s = 0; s < segments; ++s)
+    for (int r = 0; r < rings; ++r) {
+      const int a = vid(s, r), b = vid(s + 1, r), c = vid(s + 1, r + 1), d = vid(s, r + 1);
+      m.faces.insert(m.faces.end(), {a, b, c, a, c, d});
+    }
+  mesh_finalize(m);
+  return m;
+}
+
+Model model_from_mesh(const ObjMesh& mesh, int V, int H, uint64_t seed) {
+  Aabb b;
+  for (int a = 0; a < 3; ++a) {
+    b.mn[a] = std::numeric_limits<float>::max();
+    b.mx[a] = std::numeric_limits<float>::lowest();
+  }
+  for (size_t i = 0; i < mesh.verts.size() / 3; ++i)
+    for (int a = 0; a < 3; ++a) {
+      b.mn[a] = std::min(b.mn[a], mesh.verts[3 * i + a]);
+      b.mx[a] = std::max(b.mx[a], mesh.verts[3 * i + a]);
+    }
+  const Aabb frame = inflate_frame(b);
+  Model m;
+  m.voxel_res = V;
+  m.hit_cap = H;
+  m.n_levels = 2;
+  m.f_dim = 3;
+  m.table_size = 1u << 17;
+  m.hidden = 128;
+  m.n_mat = mesh.n_mat;
+  m.level_res = {64, 128};
+  m.occupancy = voxelize_surface(mesh.verts, mesh.faces, frame, V);
+  m.aabb = frame;
+  m.materials.assign(static_cast<size_t>(mesh.n_mat), Material{{0.7f, 0.7f, 0.7f}, 0u, 0.5f});
+  init_random_model(m, seed);
+  return m;
+}
+
+// ----------------------------------------------------------- scene query
+
+// object_space_ray (renderer.cpp:30-37): Eigen Affine3f * point = linear*p +
+// translation with the product summed over the inner index in order.
+static Ray object_space_ray(const float w2o[12], const Ray& r, float t_max) {
+  Ray o;
+  for (int i = 0; i < 3; ++i) {
+    const float* L = w2o + 4 * i;
+    o.o[i] = ((L[0] * r.o[0] + L[1] * r.o[1]) + L[2] * r.o[2]) + L[3];
+    o.d[i] = (L[0] * r.d[0] + L[1] * r.d[1]) + L[2] * r.d[2];
+  }
+  o.t_min = r.t_min;
+  o.t_max = t_max;
+  return o;
+}
+
+void scene_query(const Instance* inst, int n_inst, const Ray* rays, int64_t n, int mode,
+                 SceneHit* out, int workers) {
+  const float inf = std::numeric_limits<float>::infinity();
+  for (int64_t i = 0; i < n; ++i) {
+    out[i] = SceneHit{};
+    out[i].t = rays[i].t_max;  // best_t with no triangle objects (renderer.cpp:275, 314)
+    out[i].object_index = -1;
+  }
+  // Pairs in stable object order (renderer.cpp:175-179): object-major loop.
+  std::vector<Ray> oray;
+  std::vector<int64_t> slot;
+  std::vector<HitRecord> hits;
+  for (int k = 0; k < n_inst; ++k) {
+    const Model& m = *inst[k].model;
+    oray.clear();
+    slot.clear();
+    for (int64_t i = 0; i < n; ++i) {
+      // collect_pairs: interval on the unclipped object-space ray, kept iff
+      // enter < max_t (renderer.cpp:165-172); max_t = t_max (no triangles)
+      Ray o = object_space_ray(inst[k].w2o, rays[i], inf);
+      Interval iv;
+      if (!ray_aabb_intersect(o, m.aabb, &iv) || !(iv.enter < rays[i].t_max)) continue;
+      o.t_max = rays[i].t_max;  // carries the pair gate into narrow_phase
+      oray.push_back(o);
+      slot.push_back(i);
+    }
+    hits.assign(oray.size(), HitRecord{});
+    narrow_phase(m, oray.data(), static_cast<int64_t>(oray.size()), mode, hits.data(), workers);
+    for (size_t p = 0; p < oray.size(); ++p) {
+      const HitRecord& h = hits[p];
+      if (!(h.flags_material & 2u)) continue;  // !nh.occluded
+      const Ray& ray = rays[slot[p]];
+      SceneHit& sh = out[slot[p]];
+      const float t = h.t_world;
+      if (mode == kClosest) {
+        if (t >= sh.t || t < ray.t_min) continue;  // renderer.cpp:284
+        sh.t = t;
+        for (int a = 0; a < 3; ++a) sh.position[a] = ray.o[a] + t * ray.d[a];  // Ray::at
+        const float* n0 = h.normal;
+        float nw[3];
+        if (n0[0] * n0[0] + n0[1] * n0[1] + n0[2] * n0[2] == 0.0f) {
+          for (int a = 0; a < 3; ++a) nw[a] = -ray.d[a];
+        } else {  // normal_to_world: (W2O.linear^T n).normalized()
+          const float* L = inst[k].w2o;
+          for (int a = 0; a < 3; ++a) nw[a] = (L[a] * n0[0] + L[4 + a] * n0[1]) + L[8 + a] * n0[2];
+          const float len = std::sqrt((nw[0] * nw[0] + nw[1] * nw[1]) + nw[2] * nw[2]);
+          if (len > 0.0f)
+            for (int a = 0; a < 3; ++a) nw[a] = nw[a] / len;
+        }
+        if ((nw[0] * ray.d[0] + nw[1] * ray.d[1]) + nw[2] * ray.d[2] > 0.0f)
+          for (int a = 0; a < 3; ++a) nw[a] = -nw[a];
+        for (int a = 0; a < 3; ++a) {
+          sh.normal[a] = nw[a];
+          sh.albedo[a] = h.albedo[a];
+        }
+        const int mat = std::clamp(static_cast<int>(h.flags_material >> 8), 0,
+                                   static_cast<int>(m.materials.size()) - 1);
+        sh.kind = m.materials[static_cast<size_t>(mat)].kind;
+        sh.roughness = m.materials[static_cast<size_t>(mat)].roughness;
+        sh.object_index = k;
+        sh.flags = 1u;
+      } else if (t >= ray.t_min && t <= ray.t_max) {  // renderer.cpp:319
+        sh.flags = 1u;
+        if (sh.object_index < 0) sh.object_index = k;
+      }
+    }
+  }
+}
+
 }  // namespace oracle

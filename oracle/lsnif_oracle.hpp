@@ -168,4 +168,33 @@ static_assert(sizeof(HitRecord) == 32, "HitRecord must match lsnif_hit (32 B)");
 void narrow_phase(const Model& m, const Ray* rays, int64_t n, int mode, HitRecord* out,
                   int workers);
 
+// ---- procedural fixture meshes (shapes.cpp:18-112) ----
+ObjMesh make_uv_sphere(float radius, int segments, int rings);
+ObjMesh make_box(const float half[3]);
+ObjMesh make_torus(float major_radius, float minor_radius, int segments, int rings);
+// train() setup state (T = 0) for a mesh: frame, V-voxelization, random init.
+Model model_from_mesh(const ObjMesh& mesh, int V, int H, uint64_t seed);
+
+// ---- multi-object query (renderer.cpp:154-181 collect_pairs with a
+//      brute-force broad phase, stable sort by object, run_narrow_phase per
+//      object group, accept rules 280-301 / 316-321) ----
+struct Instance {
+  const Model* model;
+  float w2o[12];  // world_to_object, row-major 3x4 [linear | translation]
+};
+struct SceneHit {   // SurfaceHit (renderer.hpp:56-65) + bookkeeping, 64 B
+  float t;
+  float position[3];
+  float normal[3];
+  float albedo[3];
+  uint32_t kind;
+  float roughness;
+  int32_t object_index;
+  uint32_t flags;   // 1 = hit (closest) / occluded (any)
+  uint32_t pad[2];
+};
+static_assert(sizeof(SceneHit) == 64, "SceneHit must match lsnif_scene_hit (64 B)");
+void scene_query(const Instance* inst, int n_inst, const Ray* rays, int64_t n, int mode,
+                 SceneHit* out, int workers);
+
 }  // namespace oracle

@@ -19,7 +19,10 @@ FAST_LIB = os.path.join(HERE, "_native", "liblsnif_oracle_fast.so")
 RAY_DTYPE = np.dtype([("o", "<f4", 3), ("d", "<f4", 3), ("t_min", "<f4"), ("t_max", "<f4")])
 HIT_DTYPE = np.dtype([("flags_material", "<u4"), ("t_world", "<f4"), ("normal", "<f4", 3),
                       ("albedo", "<f4", 3)])
-assert RAY_DTYPE.itemsize == 32 and HIT_DTYPE.itemsize == 32
+SCENE_HIT_DTYPE = np.dtype([("t", "<f4"), ("position", "<f4", 3), ("normal", "<f4", 3),
+                            ("albedo", "<f4", 3), ("kind", "<u4"), ("roughness", "<f4"),
+                            ("object_index", "<i4"), ("flags", "<u4"), ("pad", "<u4", 2)])
+assert RAY_DTYPE.itemsize == 32 and HIT_DTYPE.itemsize == 32 and SCENE_HIT_DTYPE.itemsize == 64
 
 _P = C.c_void_p
 
@@ -68,6 +71,8 @@ def _load(path: str) -> C.CDLL:
     f.oracle_time_narrow_phase.restype = C.c_double
     f.oracle_time_narrow_phase.argtypes = [_P, _P, C.c_int64, C.c_int, _P, C.c_int, C.c_int]
     f.oracle_trace.argtypes = [_P, _P, C.c_int64] + [_P] * 7
+    f.oracle_build_shape_model.argtypes = [C.c_int, C.c_uint64, C.c_char_p]
+    f.oracle_scene_query.argtypes = [_P, _P, C.c_int, _P, C.c_int64, C.c_int, _P, C.c_int]
     return lib
 
 
@@ -201,6 +206,24 @@ class OracleModel:
 def build_obj_model(obj_path: str, out_path: str, V: int = 32, H: int = 18, seed: int = 0) -> None:
     L = lib()
     _check(L.oracle_build_obj_model(obj_path.encode(), V, H, seed, out_path.encode()), L)
+
+
+def scene_query(models, w2o, rays: np.ndarray, mode: int = 0, workers: int = 0) -> np.ndarray:
+    """Multi-object query (collect_pairs + per-object narrow phase + accept,
+    renderer.cpp:154-323) over instances (models[k], w2o[k] 3x4)."""
+    L = models[0].L
+    rays = np.ascontiguousarray(rays, RAY_DTYPE)
+    handles = (C.c_void_p * len(models))(*[m.h for m in models])
+    w = np.ascontiguousarray(np.asarray(w2o, np.float32).reshape(len(models), 12))
+    out = np.zeros(len(rays), SCENE_HIT_DTYPE)
+    _check(L.oracle_scene_query(C.cast(handles, C.c_void_p), _ptr(w), len(models), _ptr(rays),
+                                len(rays), mode, _ptr(out), workers), L)
+    return out
+
+
+def build_shape_model(shape: int, seed: int, out_path: str) -> None:
+    L = lib()
+    _check(L.oracle_build_shape_model(shape, seed, out_path.encode()), L)
 
 
 def dda_local(o, d, t_min, t_max, occ: np.ndarray, res: int, cap: int):

@@ -341,4 +341,30 @@ int oracle_trace(void* mp, const Ray* rays, int64_t n, int32_t* info, float* int
   });
 }
 
+// Procedural fixture model (shapes.cpp) -> train() setup state -> file.
+// shape: 0 sphere, 1 box, 2 torus.
+int oracle_build_shape_model(int shape, uint64_t seed, const char* out_path) {
+  return guarded([&] {
+    ObjMesh mesh;
+    if (shape == 0) mesh = make_uv_sphere(1.0f, 32, 16);
+    else if (shape == 1) {
+      const float h[3] = {1.0f, 0.6f, 0.8f};
+      mesh = make_box(h);
+    } else mesh = make_torus(1.0f, 0.35f, 48, 24);
+    save_model(model_from_mesh(mesh, 32, 18, seed), out_path);
+  });
+}
+
+int oracle_scene_query(void** models, const float* w2o, int n_inst, const Ray* rays, int64_t n,
+                       int mode, SceneHit* out, int workers) {
+  return guarded([&] {
+    std::vector<Instance> inst(static_cast<size_t>(n_inst));
+    for (int k = 0; k < n_inst; ++k) {
+      inst[static_cast<size_t>(k)].model = static_cast<Model*>(models[k]);
+      std::memcpy(inst[static_cast<size_t>(k)].w2o, w2o + 12 * k, 48);
+    }
+    scene_query(inst.data(), n_inst, rays, n, mode, out, workers);
+  });
+}
+
 }  // extern "C"

@@ -411,6 +411,13 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
     std::memcpy(&m.occ_threshold, &hi, 4);
   }
 
+  {  // material table (model_io.cpp:159-164); one default entry if empty
+    std::vector<lsnif_material> mats(d.materials, d.materials + std::max(d.n_materials, 0));
+    if (mats.empty()) mats.push_back(lsnif_material{{0.7f, 0.7f, 0.7f}, 0u, 0.5f});
+    m.materials = M.upload<lsnif_material>(mats.data(), mats.size() * sizeof(lsnif_material));
+    m.n_materials = static_cast<int>(mats.size());
+  }
+
   M.info.voxel_res = V;
   M.info.hit_cap = H;
   M.info.n_levels = L;
@@ -530,8 +537,9 @@ void create_into(const lsnif_model_desc& d, int device, lsnif_model* out) {
   *out = M.release();
 }
 
+// n is the ray count, or its upper bound when n_dev (device-side count) is set.
 void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, lsnif_hit* d_hits,
-               cudaStream_t st) {
+               cudaStream_t st, const int32_t* n_dev = nullptr) {
   if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
   if (mode != LSNIF_QUERY_CLOSEST && mode != LSNIF_QUERY_ANY) fail(LSNIF_INVALID_ARGUMENT, "bad query mode");
   if (n > 0 && (!d_rays || !d_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
@@ -547,6 +555,8 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     tp.m = M.dm;
     tp.rays = d_rays + s;
     tp.n = cn;
+    tp.n_dev = n_dev;
+    tp.offset = s;
     tp.mode = mode;
     tp.out = d_hits + s;
     tp.X = w.X;
@@ -592,9 +602,101 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
 
 }  // namespace
 
+struct lsnif_scene_s {
+  int device = 0;
+  std::vector<lsnif_model> models;
+  std::vector<lsnif_dev::InstanceParams> inst;
+  struct Scratch {
+    lsnif_ray* orays = nullptr;
+    int32_t* slots = nullptr;
+    lsnif_hit* hits = nullptr;
+    int32_t* count = nullptr;
+    int64_t cap = 0;
+    ~Scratch() {
+      cudaFree(orays);
+      cudaFree(slots);
+      cudaFree(hits);
+      cudaFree(count);
+    }
+  };
+  std::mutex mu;
+  std::map<cudaStream_t, std::unique_ptr<Scratch>> scratch;
+
+  Scratch& get(cudaStream_t st, int64_t n) {
+    std::lock_guard<std::mutex> lock(mu);
+    auto& s = scratch[st];
+    if (!s) {
+      s = std::make_unique<Scratch>();
+      ck(cudaMalloc(&s->count, 64), "cudaMalloc(scene count)");
+    }
+    if (n > s->cap) {
+      cudaFree(s->orays);
+      cudaFree(s->slots);
+      cudaFree(s->hits);
+      s->orays = nullptr;
+      s->slots = nullptr;
+      s->hits = nullptr;
+      ck(cudaMalloc(&s->orays, n * sizeof(lsnif_ray)), "cudaMalloc(scene rays)");
+      ck(cudaMalloc(&s->slots, n * sizeof(int32_t)), "cudaMalloc(scene slots)");
+      ck(cudaMalloc(&s->hits, n * sizeof(lsnif_hit)), "cudaMalloc(scene hits)");
+      s->cap = n;
+    }
+    return *s;
+  }
+};
+
 extern "C" {
 
 const char* lsnif_last_error(void) { return g_err.c_str(); }
+
+lsnif_status lsnif_scene_create(const lsnif_instance* instances, int32_t n, lsnif_scene* out) {
+  return guarded([&] {
+    if (!out) fail(LSNIF_INVALID_ARGUMENT, "null output handle");
+    if (n < 0 || (n > 0 && !instances)) fail(LSNIF_INVALID_ARGUMENT, "bad instance list");
+    auto S = std::make_unique<lsnif_scene_s>();
+    for (int32_t k = 0; k < n; ++k) {
+      check_model(instances[k].model);
+      if (k > 0 && instances[k].model->device != instances[0].model->device)
+        fail(LSNIF_INVALID_ARGUMENT, "scene instances must share one device");
+      lsnif_dev::InstanceParams ip{};
+      std::memcpy(ip.w2o, instances[k].world_to_object, sizeof(ip.w2o));
+      ip.index = k;
+      S->models.push_back(instances[k].model);
+      S->inst.push_back(ip);
+    }
+    S->device = n > 0 ? instances[0].model->device : 0;
+    *out = S.release();
+  });
+}
+
+lsnif_status lsnif_scene_destroy(lsnif_scene scene) {
+  return guarded([&] { delete scene; });
+}
+
+lsnif_status lsnif_scene_query(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n, int mode,
+                               lsnif_scene_hit* d_hits, void* stream) {
+  return guarded([&] {
+    if (!scene) fail(LSNIF_INVALID_ARGUMENT, "null scene");
+    if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
+    if (mode != LSNIF_QUERY_CLOSEST && mode != LSNIF_QUERY_ANY) fail(LSNIF_INVALID_ARGUMENT, "bad query mode");
+    if (n > 0 && (!d_rays || !d_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
+    if (n > INT32_MAX) fail(LSNIF_INVALID_ARGUMENT, "more than 2^31-1 rays in one call");
+    if (n == 0) return;
+    ck(cudaSetDevice(scene->device), "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto& S = scene->get(st, n);
+    ck(lsnif_dev::launch_scene_init(d_rays, n, d_hits, st), "scene_init_kernel");
+    for (size_t k = 0; k < scene->inst.size(); ++k) {  // object order (renderer.cpp:175-179)
+      lsnif_model_s& M = *scene->models[k];
+      ck(cudaMemsetAsync(S.count, 0, 4, st), "cudaMemsetAsync");
+      ck(lsnif_dev::launch_broad_phase(M.dm, scene->inst[k], d_rays, n, S.orays, S.slots, S.count, st),
+         "broad_phase_kernel");
+      run_query(M, S.orays, n, mode, S.hits, st, S.count);
+      ck(lsnif_dev::launch_merge(M.dm, scene->inst[k], d_rays, S.hits, S.slots, S.count, n, mode, d_hits, st),
+         "merge_kernel");
+    }
+  });
+}
 
 const char* lsnif_build_info(void) {
   return "liblsnif_gpu sm_100a: trace_encode_kernel + mlp_tc_kernel (tcgen05 kind::f16, TMEM), "

@@ -44,6 +44,8 @@ struct DevModel {
   const float* w_f32;                  // w1 | b1 | w2 | b2 | w3 | b3 (decoded fp32, row-major)
   float act_scale, inv_act_scale;      // power of two
   float occ_threshold;                 // smallest z with 1/(1+expf(-z)) > 0.5 under the host libm
+  const lsnif_material* materials;     // material table (model_io.cpp:159-164)
+  int n_materials;
   float z_zero[32];                    // logits of the all-zero input (rays without points)
 };
 

@@ -47,7 +47,9 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
   const float scale = m.act_scale;
   const int64_t nbatch = (P.n + 127) / 128;
   uint32_t st_pair = 0, st_rows = 0, st_pts = 0, st_vol = 0;  // query statistics
-  const int64_t nwb = (P.n + 31) / 32;  // 32-ray warp batches, fetched dynamically
+  const int64_t n_rays = P.n_dev ? max(static_cast<int64_t>(0), min(P.n, static_cast<int64_t>(*P.n_dev) - P.offset))
+                                 : P.n;
+  const int64_t nwb = (n_rays + 31) / 32;  // 32-ray warp batches, fetched dynamically
 
   // Each warp claims 32-ray batches from a global counter; the next claim
   // and the next batch's ray loads are issued before the current batch is
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
   float4 nra = make_float4(0, 0, 0, 0), nrb = nra;
   auto load_ray = [&](int64_t wb) {
     const int64_t r = wb * 32 + lane;
-    if (wb < nwb && r < P.n) {
+    if (wb < nwb && r < n_rays) {
       const float4* r4 = reinterpret_cast<const float4*>(P.rays + r);
       nra = __ldg(r4);
       nrb = __ldg(r4 + 1);
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
   while (next_wb < nwb) {
     const int64_t wbatch = next_wb;
     const int64_t ray_idx = wbatch * 32 + lane;
-    const bool live = ray_idx < P.n;
+    const bool live = ray_idx < n_rays;
     const float4 ra = nra, rb = nrb;
     next_wb = claim();
     load_ray(next_wb);
@@ -516,6 +518,139 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, 2 * HID);
   }
+}
+
+// ===================================================== multi-object scenes
+
+// best_t = ray.t_max (no triangle objects, renderer.cpp:275), no hit.
+__global__ void scene_init_kernel(const lsnif_ray* __restrict__ rays, int64_t n, lsnif_scene_hit* out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float4* o = reinterpret_cast<float4*>(out + i);
+  const float t_max = rays[i].t_max;
+  o[0] = make_float4(t_max, 0.f, 0.f, 0.f);
+  o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+  o[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+  o[3] = make_float4(0.f, __int_as_float(-1), 0.f, 0.f);
+}
+
+// object_space_ray (renderer.cpp:30-37): linear*p + translation, inner sum in
+// index order, unfused.
+__device__ __forceinline__ void to_object(const float* L, const float p[3], const float d[3], float op[3],
+                                          float od[3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const float* r = L + 4 * i;
+    op[i] = __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(r[0], p[0]), __fmul_rn(r[1], p[1])), __fmul_rn(r[2], p[2])), r[3]);
+    od[i] = __fadd_rn(__fadd_rn(__fmul_rn(r[0], d[0]), __fmul_rn(r[1], d[1])), __fmul_rn(r[2], d[2]));
+  }
+}
+
+// collect_pairs (renderer.cpp:159-173) for one instance: object-space ray,
+// interval on the frame box with t_max = inf, kept iff enter < max_t.
+// Emits the compacted object-space rays (t_max = the pair gate) + slots.
+__global__ void __launch_bounds__(256) broad_phase_kernel(const DevModel m, const InstanceParams ip,
+                                                          const lsnif_ray* __restrict__ rays, int64_t n,
+                                                          lsnif_ray* __restrict__ orays, int32_t* __restrict__ slots,
+                                                          int32_t* count) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  bool keep = false;
+  float op[3], od[3], t_min = 0.f, t_max = 0.f;
+  if (i < n) {
+    const float4* r4 = reinterpret_cast<const float4*>(rays + i);
+    const float4 a = __ldg(r4), b = __ldg(r4 + 1);
+    const float p[3] = {a.x, a.y, a.z}, d[3] = {a.w, b.x, b.y};
+    t_min = b.z;
+    t_max = b.w;
+    to_object(ip.w2o, p, d, op, od);
+    float enter, exit;
+    keep = frame_interval(m, op, od, t_min, t_max, enter, exit);
+  }
+  const unsigned mask = __ballot_sync(0xffffffffu, keep);
+  int base = 0;
+  if (lane == 0 && mask) base = atomicAdd(count, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (keep) {
+    const int j = base + __popc(mask & ((1u << lane) - 1u));
+    float4* dst = reinterpret_cast<float4*>(orays + j);
+    dst[0] = make_float4(op[0], op[1], op[2], od[0]);
+    dst[1] = make_float4(od[1], od[2], t_min, t_max);
+    slots[j] = static_cast<int32_t>(i);
+  }
+}
+
+// Accept + merge of one instance's neural hits into the scene result, in
+// object order (renderer.cpp:280-301 closest, 316-321 any): each ray occurs
+// at most once per instance list, so no atomics are needed.
+__global__ void __launch_bounds__(256) merge_kernel(const DevModel m, const InstanceParams ip,
+                                                    const lsnif_ray* __restrict__ rays,
+                                                    const lsnif_hit* __restrict__ hits,
+                                                    const int32_t* __restrict__ slots, const int32_t* count,
+                                                    int mode, lsnif_scene_hit* out) {
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= *count) return;
+  const lsnif_hit h = hits[j];
+  if (!(h.flags_material & LSNIF_HIT_OCCLUDED)) return;
+  const int32_t slot = slots[j];
+  const lsnif_ray r = rays[slot];
+  lsnif_scene_hit& sh = out[slot];
+  const float t = h.t_world;
+  if (mode == LSNIF_QUERY_CLOSEST) {
+    if (t >= sh.t || t < r.t_min) return;
+    lsnif_scene_hit o{};
+    o.t = t;
+    for (int a = 0; a < 3; ++a) o.position[a] = __fadd_rn(r.origin[a], __fmul_rn(t, r.direction[a]));
+    const float* n0 = h.normal;
+    float nw[3];
+    const float nn = __fadd_rn(__fadd_rn(__fmul_rn(n0[0], n0[0]), __fmul_rn(n0[1], n0[1])), __fmul_rn(n0[2], n0[2]));
+    if (nn == 0.0f) {
+      for (int a = 0; a < 3; ++a) nw[a] = -r.direction[a];
+    } else {  // normal_to_world (renderer.cpp:39-41): (W2O.linear^T n).normalized()
+      const float* L = ip.w2o;
+      for (int a = 0; a < 3; ++a)
+        nw[a] = __fadd_rn(__fadd_rn(__fmul_rn(L[a], n0[0]), __fmul_rn(L[4 + a], n0[1])), __fmul_rn(L[8 + a], n0[2]));
+      const float len = sqrtf(__fadd_rn(__fadd_rn(__fmul_rn(nw[0], nw[0]), __fmul_rn(nw[1], nw[1])), __fmul_rn(nw[2], nw[2])));
+      if (len > 0.0f)
+        for (int a = 0; a < 3; ++a) nw[a] = __fdiv_rn(nw[a], len);
+    }
+    const float dd = __fadd_rn(__fadd_rn(__fmul_rn(nw[0], r.direction[0]), __fmul_rn(nw[1], r.direction[1])),
+                               __fmul_rn(nw[2], r.direction[2]));
+    for (int a = 0; a < 3; ++a) {
+      o.normal[a] = dd > 0.0f ? -nw[a] : nw[a];
+      o.albedo[a] = h.albedo[a];
+    }
+    const int mat = iclamp(static_cast<int>(h.flags_material >> LSNIF_HIT_MATERIAL_SHIFT), 0, m.n_materials - 1);
+    o.kind = m.materials[mat].kind;
+    o.roughness = m.materials[mat].roughness;
+    o.object_index = ip.index;
+    o.flags = 1u;
+    sh = o;
+  } else if (t >= r.t_min && t <= r.t_max) {
+    sh.flags = 1u;
+    if (sh.object_index < 0) sh.object_index = ip.index;
+  }
+}
+
+cudaError_t launch_scene_init(const lsnif_ray* rays, int64_t n, lsnif_scene_hit* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  scene_init_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(rays, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_broad_phase(const DevModel& m, const InstanceParams& ip, const lsnif_ray* rays, int64_t n,
+                               lsnif_ray* orays, int32_t* slots, int32_t* count, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  broad_phase_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(m, ip, rays, n, orays, slots, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_merge(const DevModel& m, const InstanceParams& ip, const lsnif_ray* rays,
+                         const lsnif_hit* hits, const int32_t* slots, const int32_t* count, int64_t n_max,
+                         int mode, lsnif_scene_hit* out, cudaStream_t st) {
+  if (n_max <= 0) return cudaSuccess;
+  merge_kernel<<<static_cast<unsigned>((n_max + 255) / 256), 256, 0, st>>>(m, ip, rays, hits, slots, count, mode, out);
+  return cudaGetLastError();
 }
 
 // ==================================================== fp32 infer_batch

@@ -26,6 +26,9 @@ LIB_PATH = os.path.join(HERE, "liblsnif_gpu.so")
 RAY_DTYPE = np.dtype([("o", "<f4", 3), ("d", "<f4", 3), ("t_min", "<f4"), ("t_max", "<f4")])
 HIT_DTYPE = np.dtype([("flags_material", "<u4"), ("t_world", "<f4"), ("normal", "<f4", 3),
                       ("albedo", "<f4", 3)])
+SCENE_HIT_DTYPE = np.dtype([("t", "<f4"), ("position", "<f4", 3), ("normal", "<f4", 3),
+                            ("albedo", "<f4", 3), ("kind", "<u4"), ("roughness", "<f4"),
+                            ("object_index", "<i4"), ("flags", "<u4"), ("pad", "<u4", 2)])
 PAIR, OCCLUDED, ACCEPTED = 1, 2, 4
 CLOSEST, ANY = 0, 1
 
@@ -78,10 +81,14 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.lsnif_debug_traverse.argtypes = [P, P, C.c_int64] + [P] * 7 + [P]
     lib.lsnif_last_query_stats.argtypes = [P, P, C.POINTER(QueryStats)]
     lib.lsnif_profile_enable.argtypes = [P, C.c_int]
+    lib.lsnif_scene_create.argtypes = [P, C.c_int32, C.POINTER(P)]
+    lib.lsnif_scene_destroy.argtypes = [P]
+    lib.lsnif_scene_query.argtypes = [P, P, C.c_int64, C.c_int, P, P]
     lib.lsnif_profile_read.argtypes = [P, P, C.c_int, C.POINTER(Profile)]
     for name in ("lsnif_model_load", "lsnif_model_destroy", "lsnif_model_get_info", "lsnif_query",
                  "lsnif_query_host", "lsnif_infer_batch", "lsnif_debug_traverse",
-                 "lsnif_last_query_stats", "lsnif_profile_enable", "lsnif_profile_read"):
+                 "lsnif_last_query_stats", "lsnif_profile_enable", "lsnif_profile_read",
+                 "lsnif_scene_create", "lsnif_scene_destroy", "lsnif_scene_query"):
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -217,6 +224,53 @@ class GpuModel:
         """occluded_batch semantics: 1 where a neural hit lies in [t_min, t_max]."""
         h = self.query_host(rays, ANY)
         return ((h["flags_material"] & ACCEPTED) != 0).astype(np.int8)
+
+
+class Instance(C.Structure):
+    _fields_ = [("model", C.c_void_p), ("world_to_object", C.c_float * 12)]
+
+
+class GpuScene:
+    """Multi-object LSNIF scene: instances (model, world_to_object 3x4) in
+    object order — the LSNIF part of PreparedScene (renderer.hpp:67-131)."""
+
+    def __init__(self, instances):
+        self._models = [m for m, _ in instances]  # keep the models alive
+        arr = (Instance * len(instances))()
+        for k, (m, w2o) in enumerate(instances):
+            arr[k].model = m.h
+            arr[k].world_to_object[:] = [float(v) for v in np.asarray(w2o, np.float32).reshape(12)]
+        h = C.c_void_p()
+        _check(load_library().lsnif_scene_create(arr, len(instances), C.byref(h)))
+        self.h = h
+
+    def query(self, rays, mode: int = CLOSEST, out=None, stream=None):
+        """World-space CUDA rays (n, 8) -> (n, 16) int32 tensor of
+        lsnif_scene_hit records (view with scene_hits_to_numpy)."""
+        torch = _torch()
+        rays = rays.contiguous()
+        n = rays.shape[0]
+        if out is None:
+            out = torch.empty((n, 16), dtype=torch.int32, device=rays.device)
+        _check(load_library().lsnif_scene_query(self.h, rays.data_ptr(), n, mode, out.data_ptr(),
+                                                _stream_ptr(stream)))
+        return out
+
+    def close(self):
+        if getattr(self, "h", None):
+            load_library().lsnif_scene_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def scene_hits_to_numpy(hits) -> np.ndarray:
+    a = hits.detach().cpu().numpy() if hasattr(hits, "detach") else np.asarray(hits)
+    return np.ascontiguousarray(a).view(SCENE_HIT_DTYPE).reshape(-1)
 
 
 def load_model(path: str, device: int = 0) -> GpuModel:

@@ -138,3 +138,30 @@ def shadow_rays(primary: np.ndarray, hits: np.ndarray, box: np.ndarray,
     rays["t_min"] = 0.0
     rays["t_max"] = dist[keep] * f32(1 - 1e-4)
     return rays, idx[keep]
+
+
+# ---------------------------------------------------------------- C4 scene
+
+C4_MODELS = ["teapot_seed0", "sphere_seed1", "torus_seed2", "box_seed3"]
+C4_INSTANCES = [0, 1, 2, 3, 2, 0, 1, 0]   # model per instance: teapot x3, sphere x2, torus x2, box
+C4_CAMERA = dict(position=(0.0, 7.0, 16.0), look_at=(0.0, 0.5, 0.0), up=(0.0, 1.0, 0.0),
+                 vfov_deg=45.0)
+
+
+def c4_world_to_object() -> np.ndarray:
+    """(8, 3, 4) float32 world_to_object of the C4 instances: a 4x2 grid with
+    4-unit spacing, yaw 0 / 45 degrees alternating."""
+    out = np.zeros((8, 3, 4), np.float32)
+    for i in range(8):
+        pos = np.array([(i % 4 - 1.5) * 4.0, 0.0, (i // 4 - 0.5) * 4.0])
+        yaw = math.radians(45.0 if i % 2 else 0.0)
+        c, s = math.cos(yaw), math.sin(yaw)
+        R = np.array([[c, 0, s], [0, 1, 0], [-s, 0, c]])   # object -> world rotation
+        Rt = R.T                                            # world -> object
+        out[i, :, :3] = Rt
+        out[i, :, 3] = -Rt @ pos
+    return out
+
+
+def c4_bounds() -> np.ndarray:
+    return np.array([-8.5, -1.5, -4.5, 8.5, 2.5, 4.5], np.float32)

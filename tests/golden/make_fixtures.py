@@ -6,6 +6,11 @@ container, where /root/reference exists):
                       surface voxelization, random-init hash grid (M=2^17,
                       levels 64/128, F=3) and MLP (108-128-128-10) from seed 0,
                       saved in the LSNF v1 format (model_io.cpp:71-114).
+  sphere_seed1.lsnif, torus_seed2.lsnif, box_seed3.lsnif
+                      the same setup state for the procedural fixtures of
+                      shapes.cpp (make_uv_sphere(1,32,16), make_torus(1,.35,48,24),
+                      make_box((1,.6,.8))) with seeds 1, 2, 3 — the C4 scene's
+                      other objects.
 """
 import os
 import sys
@@ -20,3 +25,7 @@ if __name__ == "__main__":
     out = os.path.join(HERE, "teapot_seed0.lsnif")
     oracle.build_obj_model(REF_OBJ, out, V=32, H=18, seed=0)
     print("wrote", out, os.path.getsize(out), "bytes")
+    for shape, seed, name in [(0, 1, "sphere_seed1"), (2, 2, "torus_seed2"), (1, 3, "box_seed3")]:
+        p = os.path.join(HERE, name + ".lsnif")
+        oracle.build_shape_model(shape, seed, p)
+        print("wrote", p, os.path.getsize(p), "bytes")

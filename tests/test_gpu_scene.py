@@ -1,0 +1,70 @@
+"""GPU parity of the multi-object path: 8
+instances of 4 models under 3x4 world_to_object transforms; broad phase,
+per-object narrow phase in object order, closest-hit / any-hit merge,
+against the oracle's restatement of collect_pairs + run_narrow_phase +
+the accept rules (renderer.cpp:154-323)."""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2504_21627_b200 import lsnif, workloads as W  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module")
+def scenes():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from oracle import oracle as O
+    gm = [lsnif.GpuModel(os.path.join(GOLD, n + ".lsnif")) for n in W.C4_MODELS]
+    om = [O.OracleModel.load(os.path.join(GOLD, n + ".lsnif")) for n in W.C4_MODELS]
+    w2o = W.c4_world_to_object()
+    gs = lsnif.GpuScene([(gm[k], w2o[i]) for i, k in enumerate(W.C4_INSTANCES)])
+    return gs, [om[k] for k in W.C4_INSTANCES], w2o, O
+
+
+@pytest.mark.parametrize("which,mode", [("camera", 0), ("incoherent", 0), ("incoherent", 1)])
+def test_scene_parity(scenes, which, mode):
+    gs, om, w2o, O = scenes
+    rays = (W.camera_rays(480, 270, camera=W.C4_CAMERA) if which == "camera"
+            else W.incoherent_rays(40000, W.c4_bounds(), seed=4))
+    ref = O.scene_query(om, w2o, rays, mode, 0)
+    got = lsnif.scene_hits_to_numpy(gs.query(lsnif.rays_to_tensor(rays), mode))
+    agree_flag = np.mean(got["flags"] == ref["flags"])
+    agree_obj = np.mean(got["object_index"] == ref["object_index"])
+    assert agree_flag >= 0.999 and agree_obj >= 0.999, (agree_flag, agree_obj)
+    assert (ref["flags"] == 1).sum() > 100
+    if mode == 0:
+        both = (got["flags"] == 1) & (ref["flags"] == 1) & (got["object_index"] == ref["object_index"])
+        # t tolerance: 2e-3 of the object's frame-box interval, bounded by its world diagonal
+        assert np.all(np.abs(got["t"][both] - ref["t"][both]) <= 2e-3 * 4.0)
+        assert np.all(np.linalg.norm(got["position"][both] - ref["position"][both], axis=1) <= 1e-2)
+        cosang = np.sum(got["normal"][both] * ref["normal"][both], axis=1)
+        assert np.all(cosang >= np.cos(np.deg2rad(1.0)))
+        assert np.all(np.abs(got["albedo"][both] - ref["albedo"][both]) <= 2e-3)
+        assert np.array_equal(got["kind"][both], ref["kind"][both])
+        assert np.array_equal(got["roughness"][both], ref["roughness"][both])
+        miss = ref["flags"] == 0
+        assert np.array_equal(got["t"][miss], rays["t_max"][miss])  # best_t untouched
+
+
+def test_scene_single_instance_matches_query(scenes):
+    """One identity instance == the single-object query's accepted hits."""
+    gs, om, w2o, O = scenes
+    m = lsnif.GpuModel(os.path.join(GOLD, "teapot_seed0.lsnif"))
+    eye = np.zeros((3, 4), np.float32)
+    eye[:, :3] = np.eye(3)
+    s1 = lsnif.GpuScene([(m, eye)])
+    rays = W.camera_rays(256, 256)
+    t = lsnif.rays_to_tensor(rays)
+    sh = lsnif.scene_hits_to_numpy(s1.query(t, 0))
+    h = lsnif.hits_to_numpy(m.query(t, 0))
+    acc = (h["flags_material"] & 4) != 0
+    assert np.array_equal(sh["flags"] == 1, acc)
+    assert np.array_equal(sh["t"][acc], h["t_world"][acc])
+    assert np.array_equal(sh["albedo"][acc], h["albedo"][acc])
