@@ -44,6 +44,9 @@ WORKLOADS = {
     "c3": "C3 (configs[2]): teapot LSNIF, 16,777,216 incoherent rays (origins uniform in "
           "the frame box, directions uniform on S^2, seed 3), closest-hit, per GPU",
     "c1": "C1 (configs[0]): teapot LSNIF, 256x256 pixel-centre primary rays, closest-hit",
+    "c4": "C4 (configs[3]): 8 LSNIF instances (teapot x3, sphere x2, torus x2, box; "
+          "per-object hash grids and MLP weights, seeds 0-3) on a 4x2 grid, 1920x1080 camera "
+          "rays, brute-force broad phase + per-object narrow phase + closest-hit merge, per GPU",
     "c5": "C5 (configs[4]): teapot LSNIF, 3840x2160 x 16 spp incoherent rays (132,710,400, "
           "keyed by (pixel, sample)), closest-hit, row bands tile-sharded across the GPUs with "
           "an NCCL result gather to rank 0 inside the step (strong scaling)",
@@ -244,6 +247,62 @@ def run_reference(args, rank, world):
     return 0
 
 
+# --------------------------------------------------------------- C4 scene
+
+def run_c4(args, rank, world, dev, gpu, max_over_ranks):
+    import torch
+    from paper_2504_21627_b200 import lsnif, workloads as W
+    gold = os.path.join(ROOT, "tests", "golden")
+    models = [lsnif.GpuModel(os.path.join(gold, n + ".lsnif"), gpu) for n in W.C4_MODELS]
+    w2o = W.c4_world_to_object()
+    scene = lsnif.GpuScene([(models[k], w2o[i]) for i, k in enumerate(W.C4_INSTANCES)])
+    rays = W.camera_rays(1920, 1080, camera=W.C4_CAMERA, jitter=W.rank_jitter(rank))
+    d_rays = lsnif.rays_to_tensor(rays, dev)
+    out = torch.empty((len(rays), 16), dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        scene.query(d_rays, lsnif.CLOSEST, out=out)
+    torch.cuda.synchronize()
+    for m in models:
+        m.profile_read(reset=True, stream="all")
+        m.profile_enable(True)
+    clocks = ClockSampler(gpu)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    clocks.start()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record()
+        scene.query(d_rays, lsnif.CLOSEST, out=out)
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    clocks.stop()
+    profs = []
+    for m in models:
+        m.profile_enable(False)
+        profs.append(m.profile_read(reset=True, stream="all"))
+    elapsed_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
+    value = world * len(rays) * args.steps / (elapsed_ms / 1e3)
+    hits = lsnif.scene_hits_to_numpy(out)
+    if rank == 0:
+        tr = sum(p["trace_ms"] for p in profs) / args.steps
+        ml = sum(p["mlp_ms"] for p in profs) / args.steps
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32 traversal/encode + f16xf16->f32 tcgen05 MLP", "data": "synthetic",
+                "config": {"workload": WORKLOADS["c4"], "rays_per_step_per_gpu": len(rays),
+                           "l2": "flushed between timed steps (256 MiB write outside the events)",
+                           "parallelism": f"dp{world} (one frame per GPU)"},
+                "workload_stats": {"frac_hit": float(np.mean(hits["flags"] == 1))},
+                "kernels": {"trace_encode_kernel": {"ms_per_step": tr},
+                            "mlp_tc_kernel": {"ms_per_step": ml}},
+                "gpu_launches": sum(int(p["launches"]) for p in profs),
+                "clocks": clocks.summary()}
+        print(json.dumps(line), flush=True)
+
+
 # --------------------------------------------------------------------- ours
 
 def main():
@@ -275,6 +334,13 @@ def main():
         t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    if args.workload == "c4":
+        run_c4(args, rank, world, dev, gpu, max_over_ranks)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
 
     model = lsnif.GpuModel(MODEL_PATH, gpu)
     box = model.aabb

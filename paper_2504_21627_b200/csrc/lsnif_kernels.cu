@@ -303,18 +303,22 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
 // ============================================================ tcgen05 MLP
 
 // Warp-specialised persistent MLP over the compacted 128-row X tiles:
-//   warp 0  loader: bulk-copies X tiles into a 2-stage SMEM ring;
-//   warp 1  MMA issuer (one thread) + TMEM allocator;
-//   warps 2-5 / 6-9  two epilogue groups, ping-ponging over tiles, each with
-//           its own TMEM accumulator (128 lanes x HID cols) and SMEM hidden
-//           operand buffer, so one tile's epilogue overlaps the other's MMAs.
+//   warp 0  loader: bulk-copies X tiles into a 2-stage SMEM ring (stage =
+//           epilogue group = tile parity);
+//   warp 1  TMEM allocator + one MMA-issuing thread that polls both groups'
+//           barriers and issues whichever layer is ready (the two groups'
+//           chains are independent and only share the tensor pipe);
+//   warps 2-9 / 10-17  two epilogue groups of 8 warps (2 per TMEM lane
+//           quadrant, each taking half of the columns), each group with its
+//           own TMEM accumulator (128 lanes x HID cols) and SMEM hidden buffer.
 // Per tile: L1 = X W1^T (+b1 via the constant column), h1 = leaky(.) -> SMEM,
 // L2, h2 -> SMEM, L3 (N = 16), heads/decode/accept -> global hits.
 template <int HID>
 struct MlpLayout {
   static constexpr int kK2 = HID + 16;                      // hidden + bias block
   static constexpr uint32_t kHBytes = kTileM * kK2 * 2;     // hidden operand buffer
-  static constexpr int kThreads = 320;
+  static constexpr int kEpiWarps = 8;                       // per group
+  static constexpr int kThreads = 32 * (2 + 2 * kEpiWarps);
 };
 
 __device__ __forceinline__ void leaky_store8(const uint32_t* acc, uint8_t* dst) {
@@ -330,22 +334,37 @@ __device__ __forceinline__ void leaky_store8(const uint32_t* acc, uint8_t* dst) 
   *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(hv);
 }
 
-// h = leaky(acc) -> fp16 hidden operand row. The bias is already accumulated
-// and the activation scale carries through the positively homogeneous
-// leaky-ReLU. TMEM loads are issued two at a time (64 columns in flight).
-template <int HID>
-__device__ __forceinline__ void epi_hidden(uint32_t taddr, uint8_t* sH, int row) {
+// h = leaky(acc) -> fp16 hidden operand row, columns [c0, c0 + NC). The bias
+// is already accumulated and the activation scale carries through the
+// positively homogeneous leaky-ReLU. Two TMEM loads in flight per wait.
+template <int NC>
+__device__ __forceinline__ void epi_hidden(uint32_t taddr, uint8_t* sH, int row, int c0) {
+  uint8_t* rowp = sH + (row >> 3) * 128 + (row & 7) * 16;  // + (col >> 3) * kTileM * 16
 #pragma unroll
-  for (int cb = 0; cb < HID; cb += 64) {
+  for (int cb = 0; cb < NC; cb += 64) {
     uint32_t a0[32], a1[32];
-    tc::tmem_ld32(taddr + cb, a0);
-    tc::tmem_ld32(taddr + cb + 32, a1);
+    tc::tmem_ld32(taddr + c0 + cb, a0);
+    if (NC - cb >= 64) tc::tmem_ld32(taddr + c0 + cb + 32, a1);
     tc::tmem_wait_ld();
 #pragma unroll
-    for (int q = 0; q < 32; q += 8) leaky_store8(a0 + q, sH + canon_offset(row, cb + q, kTileM));
+    for (int q = 0; q < 32; q += 8) leaky_store8(a0 + q, rowp + ((c0 + cb + q) >> 3) * (kTileM * 16));
+    if (NC - cb >= 64) {
 #pragma unroll
-    for (int q = 0; q < 32; q += 8) leaky_store8(a1 + q, sH + canon_offset(row, cb + 32 + q, kTileM));
+      for (int q = 0; q < 32; q += 8) leaky_store8(a1 + q, rowp + ((c0 + cb + 32 + q) >> 3) * (kTileM * 16));
+    }
   }
+}
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(tc::smem_addr(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
 }
 
 template <int HID>
@@ -353,6 +372,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using Lay = MlpLayout<HID>;
   constexpr int K2 = Lay::kK2;
+  constexpr int EW = Lay::kEpiWarps;
   const DevModel& m = P.m;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t xbytes = static_cast<uint32_t>(kTileM) * m.K1P * 2;
@@ -386,15 +406,15 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       tc::mbar_init(x_full + g, 1);
       tc::mbar_init(x_empty + g, 1);
       tc::mbar_init(l_done + g, 1);
-      tc::mbar_init(h_ready + g, 128);
-      tc::mbar_init(acc_free + g, 128);
+      tc::mbar_init(h_ready + g, 32 * EW);
+      tc::mbar_init(acc_free + g, 32 * EW);
     }
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * HID);
-  if (warp >= 2) {  // bias block of both hidden buffers: col HID = act_scale, rest 0
+  if (warp >= 2 && ((warp - 2) % EW) < 4) {  // bias block of both hidden buffers
     const int row = 32 * (warp & 3) + lane;
-    const int g = (warp - 2) >> 2;
+    const int g = (warp - 2) / EW;
     const uint32_t hs = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(m.act_scale)));
     uint8_t* h = sH + g * Lay::kHBytes;
     *reinterpret_cast<uint4*>(h + canon_offset(row, HID, kTileM)) = make_uint4(hs, 0u, 0u, 0u);
@@ -429,7 +449,6 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       constexpr uint32_t kIdescH = tc::idesc_f16_f32(kTileM, HID);
       const uint32_t idesc3 = tc::idesc_f16_f32(kTileM, m.N3);
       constexpr uint32_t a_lbo = kTileM * 16;
-      uint32_t hcount[2] = {0, 0};
       auto layer = [&](uint32_t a_base, int ksteps, uint32_t b_base, uint32_t b_rows, uint32_t idesc,
                        uint32_t d) {
         tc::tc_fence_after();
@@ -439,33 +458,43 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
           tc::mma_f16_ss(d, ad, bd, idesc, ks > 0 ? 1u : 0u);
         }
       };
-      for (int i0 = 0; i0 < my_tiles; i0 += 2) {
-        const int n2 = min(2, my_tiles - i0);
-        for (int j = 0; j < n2; ++j) {  // L1 for both tiles of the pair
-          const int i = i0 + j, g = i & 1, k = i >> 1;
-          tc::mbar_wait(x_full + g, k & 1);
-          if (k > 0) tc::mbar_wait(acc_free + g, (k - 1) & 1);
-          layer(tc::smem_addr(sX + g * xstage), m.K1P / 16, sW1_a, HID, kIdescH, tmem + g * HID);
-          tc::mma_commit(x_empty + g);
-          tc::mma_commit(l_done + g);
-        }
-        for (int j = 0; j < n2; ++j) {  // L2
-          const int g = (i0 + j) & 1;
-          tc::mbar_wait(h_ready + g, hcount[g]++ & 1);
-          layer(tc::smem_addr(sH + g * Lay::kHBytes), K2 / 16, sW2_a, HID, kIdescH, tmem + g * HID);
-          tc::mma_commit(l_done + g);
-        }
-        for (int j = 0; j < n2; ++j) {  // L3
-          const int g = (i0 + j) & 1;
-          tc::mbar_wait(h_ready + g, hcount[g]++ & 1);
-          layer(tc::smem_addr(sH + g * Lay::kHBytes), K2 / 16, sW3_a, m.N3, idesc3, tmem + g * HID);
-          tc::mma_commit(l_done + g);
+      // per group: next tile index i (= g + 2k), next layer, barrier phases
+      int gi[2] = {0, 1}, gl[2] = {0, 0};
+      uint32_t hc[2] = {0, 0};
+      while (gi[0] < my_tiles || gi[1] < my_tiles) {
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          const int i = gi[g];
+          if (i >= my_tiles) continue;
+          const int k = i >> 1;
+          if (gl[g] == 0) {
+            if (!mbar_test(x_full + g, k & 1)) continue;
+            if (k > 0 && !mbar_test(acc_free + g, (k - 1) & 1)) continue;
+            layer(tc::smem_addr(sX + g * xstage), m.K1P / 16, sW1_a, HID, kIdescH, tmem + g * HID);
+            tc::mma_commit(x_empty + g);
+            tc::mma_commit(l_done + g);
+            gl[g] = 1;
+          } else {
+            if (!mbar_test(h_ready + g, hc[g] & 1)) continue;
+            ++hc[g];
+            if (gl[g] == 1) {
+              layer(tc::smem_addr(sH + g * Lay::kHBytes), K2 / 16, sW2_a, HID, kIdescH, tmem + g * HID);
+              gl[g] = 2;
+            } else {
+              layer(tc::smem_addr(sH + g * Lay::kHBytes), K2 / 16, sW3_a, m.N3, idesc3, tmem + g * HID);
+              gl[g] = 0;
+              gi[g] += 2;
+            }
+            tc::mma_commit(l_done + g);
+          }
         }
       }
     }
   } else {
     // ------------------------------------------------------------ epilogues
-    const int g = (warp - 2) >> 2;
+    const int g = (warp - 2) / EW;
+    const int e = (warp - 2) % EW;
+    const int half = e / 4;  // column half; warps e and e+4 share a lane quadrant
     const int row = 32 * (warp & 3) + lane;
     const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + g * HID;
     uint8_t* h = sH + g * Lay::kHBytes;
@@ -474,30 +503,25 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       const int tile = blockIdx.x + i * gridDim.x;
       const int grow = tile * kTileM + row;
       float4 ma = make_float4(0, 0, 0, 0), mb = ma;  // row metadata, prefetched
-      if (grow < rows) {
+      if (half == 0 && grow < rows) {
         const float4* mp = reinterpret_cast<const float4*>(P.meta + grow);
         ma = __ldg(mp);
         mb = __ldg(mp + 1);
       }
-      // layer 1 -> h1
-      tc::mbar_wait(l_done + g, lcount++ & 1);
-      tc::tc_fence_after();
-      epi_hidden<HID>(taddr, h, row);
-      tc::fence_proxy_async_smem();
-      tc::tc_fence_before();
-      tc::mbar_arrive(h_ready + g);
-      // layer 2 -> h2
-      tc::mbar_wait(l_done + g, lcount++ & 1);
-      tc::tc_fence_after();
-      epi_hidden<HID>(taddr, h, row);
-      tc::fence_proxy_async_smem();
-      tc::tc_fence_before();
-      tc::mbar_arrive(h_ready + g);
+#pragma unroll 1
+      for (int layer = 0; layer < 2; ++layer) {  // h1, h2
+        tc::mbar_wait(l_done + g, lcount++ & 1);
+        tc::tc_fence_after();
+        epi_hidden<HID / 2>(taddr, h, row, half * (HID / 2));
+        tc::fence_proxy_async_smem();
+        tc::tc_fence_before();
+        tc::mbar_arrive(h_ready + g);
+      }
       // layer 3 -> heads, decode, accept (renderer.cpp:208-223, 280-301)
       tc::mbar_wait(l_done + g, lcount++ & 1);
       tc::tc_fence_after();
       float z[16];
-      {
+      if (half == 0) {
         uint32_t acc[16];
         tc::tmem_ld16(taddr, acc);
         tc::tmem_wait_ld();
@@ -506,7 +530,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       }
       tc::tc_fence_before();
       tc::mbar_arrive(acc_free + g);
-      if (grow < rows) {
+      if (half == 0 && grow < rows) {
         lsnif_hit hh;
         decode_hit(z, m.n_mat, m.occ_threshold, ma.y, ma.z, ma.w, mb.x, P.mode, true, hh);
         store_hit(P.out + __float_as_int(ma.x), hh);
@@ -531,7 +555,7 @@ __global__ void scene_init_kernel(const lsnif_ray* __restrict__ rays, int64_t n,
   o[0] = make_float4(t_max, 0.f, 0.f, 0.f);
   o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
   o[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-  o[3] = make_float4(0.f, __int_as_float(-1), 0.f, 0.f);
+  o[3] = make_float4(__int_as_float(-1), 0.f, 0.f, 0.f);  // object_index = -1, flags = 0
 }
 
 // object_space_ray (renderer.cpp:30-37): linear*p + translation, inner sum in

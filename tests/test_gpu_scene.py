@@ -45,7 +45,12 @@ def test_scene_parity(scenes, which, mode):
         assert np.all(np.abs(got["t"][both] - ref["t"][both]) <= 2e-3 * 4.0)
         assert np.all(np.linalg.norm(got["position"][both] - ref["position"][both], axis=1) <= 1e-2)
         cosang = np.sum(got["normal"][both] * ref["normal"][both], axis=1)
-        assert np.all(cosang >= np.cos(np.deg2rad(1.0)))
+        # the face-the-ray flip (renderer.cpp:291) is discontinuous where the
+        # normal is perpendicular to the ray: allow the flipped twin there
+        ndotd = np.abs(np.sum(ref["normal"][both] * rays["d"][both], axis=1))
+        c1 = np.cos(np.deg2rad(1.0))
+        ok = (cosang >= c1) | ((ndotd < 0.02) & (np.abs(cosang) >= c1))
+        assert np.all(ok), (np.sum(~ok), cosang[~ok][:5], ndotd[~ok][:5])
         assert np.all(np.abs(got["albedo"][both] - ref["albedo"][both]) <= 2e-3)
         assert np.array_equal(got["kind"][both], ref["kind"][both])
         assert np.array_equal(got["roughness"][both], ref["roughness"][both])
