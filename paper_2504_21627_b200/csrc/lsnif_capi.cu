@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -137,7 +138,7 @@ struct HostStaging {
 
 constexpr int64_t kChunk = int64_t(1) << 21;      // rays per trace/MLP launch pair
 constexpr int64_t kHostChunk = int64_t(1) << 20;  // rays per host staging step
-constexpr size_t kMaxChunks = 1024;                // row counters per query (2^31 rays)
+constexpr size_t kMaxChunks = 4096;                // row counters per query (2^31 rays)
 // counter block, zeroed by one memset per query: 4 x u64 stats | u32 row
 // counter per chunk | u64 batch counter per chunk
 constexpr size_t kCounterBytes = 32 + 4 * kMaxChunks + 8 * kMaxChunks;
@@ -335,7 +336,7 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
 
   // UMMA canonical fp16 operands with the bias folded in as column K:
   //   W1: hid x K1P (col K1 = b1), W2: hid x (hid+16) (col hid = b2),
-  //   W3: 16 x (hid+16) (col hid = b3, rows >= n_out zero).
+  //   W3: 16 x hid (rows >= n_out zero).
   const int K2 = hid + 16;
   auto canon = [&](int rows, int cols, auto&& get) {
     std::vector<uint8_t> buf(static_cast<size_t>(rows) * cols * 2, 0);
@@ -354,11 +355,13 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
     if (c < hid) return d.w2[static_cast<size_t>(r) * hid + c];
     return c == hid ? d.b2[r] : uint16_t(0);
   });
-  const auto c3 = canon(16, K2, [&](int r, int c) -> uint16_t {
+  // W3 has no bias column: b3 is added in fp32 by the decode epilogue (an
+  // N = 16 MMA K-step costs ~50 cycles, as much as most of a layer's work)
+  const auto c3 = canon(16, hid, [&](int r, int c) -> uint16_t {
     if (r >= n_out) return 0;
-    if (c < hid) return d.w3[static_cast<size_t>(r) * hid + c];
-    return c == hid ? d.b3[r] : uint16_t(0);
+    return d.w3[static_cast<size_t>(r) * hid + c];
   });
+  for (int i = 0; i < 16; ++i) m.b3[i] = i < n_out ? b3[i] : 0.0f;
   std::vector<uint8_t> wc;
   wc.insert(wc.end(), c1.begin(), c1.end());
   wc.insert(wc.end(), c2.begin(), c2.end());
@@ -585,6 +588,7 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     mp.out = d_hits + s;
     mp.tile_bytes = M.tile_bytes();
     mp.mode = mode;
+
     if (M.profiling) {
       e0 = w.take_event();
       ck(cudaEventRecord(e0, st), "cudaEventRecord");

@@ -47,6 +47,7 @@ struct DevModel {
   const lsnif_material* materials;     // material table (model_io.cpp:159-164)
   int n_materials;
   float z_zero[32];                    // logits of the all-zero input (rays without points)
+  float b3[16];                        // output bias, added in fp32 by the decode epilogue
 };
 
 // Row bookkeeping for rays that go through the MLP.

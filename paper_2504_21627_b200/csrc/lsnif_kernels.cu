@@ -15,6 +15,8 @@
 //  infer_f32_kernel  fp32 CUDA-core infer_batch (renderer.cpp:183-226).
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include "lsnif_device.cuh"
 #include "lsnif_internal.hpp"
 #include "tc_ptx.cuh"
@@ -406,8 +408,8 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       tc::mbar_init(x_full + g, 1);
       tc::mbar_init(x_empty + g, 1);
       tc::mbar_init(l_done + g, 1);
-      tc::mbar_init(h_ready + g, 32 * EW);
-      tc::mbar_init(acc_free + g, 32 * EW);
+      tc::mbar_init(h_ready + g, EW);   // one arrival per epilogue warp
+      tc::mbar_init(acc_free + g, EW);
     }
     tc::fence_mbar_init();
   }
@@ -433,9 +435,16 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       tc::bulk_g2s(sW1, m.w_canon, m.w1_bytes, w_full);
       tc::bulk_g2s(sW2, m.w_canon + m.w1_bytes, m.w2_bytes, w_full);
       tc::bulk_g2s(sW3, m.w_canon + m.w1_bytes + m.w2_bytes, m.w3_bytes, w_full);
+      // X tiles are read once from HBM: keep kPrefetch tiles ahead in flight
+      // as L2 prefetches so the 2-stage SMEM ring is refilled from L2.
+      constexpr int kPrefetch = 6;
+      for (int i = 0; i < kPrefetch && i < my_tiles; ++i)
+        tc::bulk_prefetch_l2(P.X + static_cast<int64_t>(blockIdx.x + i * gridDim.x) * P.tile_bytes, xbytes);
       for (int i = 0; i < my_tiles; ++i) {
         const int tile = blockIdx.x + i * gridDim.x;
         const int st = i & 1, k = i >> 1;
+        if (i + kPrefetch < my_tiles)
+          tc::bulk_prefetch_l2(P.X + static_cast<int64_t>(tile + kPrefetch * gridDim.x) * P.tile_bytes, xbytes);
         if (k > 0) tc::mbar_wait(x_empty + st, (k - 1) & 1);
         tc::mbar_arrive_expect_tx(x_full + st, xbytes);
         tc::bulk_g2s(sX + st * xstage, P.X + static_cast<int64_t>(tile) * P.tile_bytes, xbytes, x_full + st);
@@ -481,7 +490,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
               layer(tc::smem_addr(sH + g * Lay::kHBytes), K2 / 16, sW2_a, HID, kIdescH, tmem + g * HID);
               gl[g] = 2;
             } else {
-              layer(tc::smem_addr(sH + g * Lay::kHBytes), K2 / 16, sW3_a, m.N3, idesc3, tmem + g * HID);
+              layer(tc::smem_addr(sH + g * Lay::kHBytes), HID / 16, sW3_a, m.N3, idesc3, tmem + g * HID);
               gl[g] = 0;
               gi[g] += 2;
             }
@@ -515,7 +524,8 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
         epi_hidden<HID / 2>(taddr, h, row, half * (HID / 2));
         tc::fence_proxy_async_smem();
         tc::tc_fence_before();
-        tc::mbar_arrive(h_ready + g);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(h_ready + g);
       }
       // layer 3 -> heads, decode, accept (renderer.cpp:208-223, 280-301)
       tc::mbar_wait(l_done + g, lcount++ & 1);
@@ -526,10 +536,11 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
         tc::tmem_ld16(taddr, acc);
         tc::tmem_wait_ld();
 #pragma unroll
-        for (int q = 0; q < 16; ++q) z[q] = __fmul_rn(__uint_as_float(acc[q]), m.inv_act_scale);
+        for (int q = 0; q < 16; ++q) z[q] = __fadd_rn(__fmul_rn(__uint_as_float(acc[q]), m.inv_act_scale), m.b3[q]);
       }
       tc::tc_fence_before();
-      tc::mbar_arrive(acc_free + g);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acc_free + g);
       if (half == 0 && grow < rows) {
         lsnif_hit hh;
         decode_hit(z, m.n_mat, m.occ_threshold, ma.y, ma.z, ma.w, mb.x, P.mode, true, hh);
