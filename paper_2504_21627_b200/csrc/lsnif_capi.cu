@@ -122,13 +122,17 @@ struct Workspace {
   }
 };
 
+// Host staging for lsnif_query_host: kSlots device buffers, each with its own
+// stream, so the H2D copy engine, the kernels and the D2H copy engine work on
+// different chunks at once (PCIe-bound; copies of a slot are stream-ordered).
+constexpr int kSlots = 4;
 struct HostStaging {
-  cudaStream_t streams[2] = {nullptr, nullptr};
-  lsnif_ray* d_rays[2] = {nullptr, nullptr};
-  lsnif_hit* d_hits[2] = {nullptr, nullptr};
+  cudaStream_t streams[kSlots] = {};
+  lsnif_ray* d_rays[kSlots] = {};
+  lsnif_hit* d_hits[kSlots] = {};
   int64_t cap = 0;
   ~HostStaging() {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kSlots; ++i) {
       cudaFree(d_rays[i]);
       cudaFree(d_hits[i]);
       if (streams[i]) cudaStreamDestroy(streams[i]);
@@ -137,7 +141,7 @@ struct HostStaging {
 };
 
 constexpr int64_t kChunk = int64_t(1) << 21;      // rays per trace/MLP launch pair
-constexpr int64_t kHostChunk = int64_t(1) << 20;  // rays per host staging step
+constexpr int64_t kHostChunk = int64_t(1) << 18;  // rays per host staging step
 constexpr size_t kMaxChunks = 4096;                // row counters per query (2^31 rays)
 // counter block, zeroed by one memset per query: 4 x u64 stats | u32 row
 // counter per chunk | u64 batch counter per chunk
@@ -753,7 +757,7 @@ lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_
     std::lock_guard<std::mutex> lock(model->staging_mu);
     if (!model->staging) {
       auto s = std::make_unique<HostStaging>();
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < kSlots; ++i) {
         ck(cudaStreamCreateWithFlags(&s->streams[i], cudaStreamNonBlocking), "cudaStreamCreate");
         ck(cudaMalloc(&s->d_rays[i], kHostChunk * sizeof(lsnif_ray)), "cudaMalloc(staging)");
         ck(cudaMalloc(&s->d_hits[i], kHostChunk * sizeof(lsnif_hit)), "cudaMalloc(staging)");
@@ -766,10 +770,10 @@ lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_
     cudaEvent_t ev;
     ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventRecord(ev, static_cast<cudaStream_t>(stream)), "cudaEventRecord");
-    for (int i = 0; i < 2; ++i) ck(cudaStreamWaitEvent(S.streams[i], ev, 0), "cudaStreamWaitEvent");
+    for (int i = 0; i < kSlots; ++i) ck(cudaStreamWaitEvent(S.streams[i], ev, 0), "cudaStreamWaitEvent");
     int64_t k = 0;
     for (int64_t s = 0; s < n; s += S.cap, ++k) {
-      const int slot = static_cast<int>(k & 1);
+      const int slot = static_cast<int>(k % kSlots);
       const int64_t cn = std::min(S.cap, n - s);
       cudaStream_t st = S.streams[slot];
       ck(cudaMemcpyAsync(S.d_rays[slot], h_rays + s, cn * sizeof(lsnif_ray), cudaMemcpyHostToDevice, st),
@@ -778,7 +782,7 @@ lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_
       ck(cudaMemcpyAsync(h_hits + s, S.d_hits[slot], cn * sizeof(lsnif_hit), cudaMemcpyDeviceToHost, st),
          "cudaMemcpyAsync(D2H)");
     }
-    for (int i = 0; i < 2; ++i) ck(cudaStreamSynchronize(S.streams[i]), "cudaStreamSynchronize");
+    for (int i = 0; i < kSlots; ++i) ck(cudaStreamSynchronize(S.streams[i]), "cudaStreamSynchronize");
     cudaEventDestroy(ev);
   });
 }
