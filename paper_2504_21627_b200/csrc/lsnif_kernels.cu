@@ -305,56 +305,49 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
 // ============================================================ tcgen05 MLP
 
 // Warp-specialised persistent MLP over the compacted 128-row X tiles:
-//   warp 0  loader: bulk-copies X tiles into a 2-stage SMEM ring (stage =
-//           epilogue group = tile parity);
+//   warp 0  loader: bulk-copies X tiles into a kXStages SMEM ring and keeps
+//           kPrefetch tiles ahead in flight as L2 prefetches;
 //   warp 1  TMEM allocator + one MMA-issuing thread that polls both groups'
-//           barriers and issues whichever layer is ready (the two groups'
-//           chains are independent and only share the tensor pipe);
+//           barriers and issues whichever layer is ready;
 //   warps 2-9 / 10-17  two epilogue groups of 8 warps (2 per TMEM lane
-//           quadrant, each taking half of the columns), each group with its
-//           own TMEM accumulator (128 lanes x HID cols) and SMEM hidden buffer.
-// Per tile: L1 = X W1^T (+b1 via the constant column), h1 = leaky(.) -> SMEM,
-// L2, h2 -> SMEM, L3 (N = 16), heads/decode/accept -> global hits.
+//           quadrant, each taking half of the columns); group g owns TMEM
+//           columns [256g, 256g+256): the fp32 accumulator D (128 cols) and
+//           the fp16 hidden operand A_h (72 cols: 128 K-values + bias block).
+// Per tile: L1 = X W1^T (A = X from SMEM, b1 via the constant column),
+// h1 = leaky(D) -> fp16 A_h (tcgen05.st), L2 = A_h W2^T (A from TMEM, b2 via
+// the constant column), h2 -> A_h, L3 = A_h W3^T (N = 16, K = 128), logits +
+// b3 in fp32, heads/decode/accept -> global hits.
 template <int HID>
 struct MlpLayout {
-  static constexpr int kK2 = HID + 16;                      // hidden + bias block
-  static constexpr uint32_t kHBytes = kTileM * kK2 * 2;     // hidden operand buffer
-  static constexpr int kEpiWarps = 8;                       // per group
+  static constexpr int kK2 = HID + 16;        // hidden + bias block
+  static constexpr int kEpiWarps = 8;         // per group
   static constexpr int kThreads = 32 * (2 + 2 * kEpiWarps);
+  static constexpr int kXStages = 4;
+  static constexpr uint32_t kGroupCols = 256; // TMEM columns per group (D + A_h)
+  static constexpr uint32_t kACol = 128;      // A_h column offset within a group
 };
 
-__device__ __forceinline__ void leaky_store8(const uint32_t* acc, uint8_t* dst) {
-  __align__(16) __half2 hv[4];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    float v0 = __uint_as_float(acc[2 * e]);
-    float v1 = __uint_as_float(acc[2 * e + 1]);
-    v0 = fmaxf(v0, __fmul_rn(v0, 0.01f));
-    v1 = fmaxf(v1, __fmul_rn(v1, 0.01f));
-    hv[e] = __floats2half2_rn(v0, v1);
-  }
-  *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(hv);
+__device__ __forceinline__ uint32_t leaky_pack(uint32_t a, uint32_t b) {
+  float v0 = __uint_as_float(a), v1 = __uint_as_float(b);
+  v0 = fmaxf(v0, __fmul_rn(v0, 0.01f));
+  v1 = fmaxf(v1, __fmul_rn(v1, 0.01f));
+  const __half2 h = __floats2half2_rn(v0, v1);
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// h = leaky(acc) -> fp16 hidden operand row, columns [c0, c0 + NC). The bias
-// is already accumulated and the activation scale carries through the
-// positively homogeneous leaky-ReLU. Two TMEM loads in flight per wait.
-template <int NC>
-__device__ __forceinline__ void epi_hidden(uint32_t taddr, uint8_t* sH, int row, int c0) {
-  uint8_t* rowp = sH + (row >> 3) * 128 + (row & 7) * 16;  // + (col >> 3) * kTileM * 16
+// h = leaky(D) for hidden columns [c0, c0 + 64) of this lane's row -> packed
+// fp16 pairs in A_h columns [c0/2, c0/2 + 32). The bias is already in D and
+// the activation scale carries through the positively homogeneous leaky-ReLU.
+__device__ __forceinline__ void epi_hidden64(uint32_t tD, uint32_t tA, int c0) {
+  uint32_t a0[32], a1[32], o[32];
+  tc::tmem_ld32(tD + c0, a0);
+  tc::tmem_ld32(tD + c0 + 32, a1);
+  tc::tmem_wait_ld();
 #pragma unroll
-  for (int cb = 0; cb < NC; cb += 64) {
-    uint32_t a0[32], a1[32];
-    tc::tmem_ld32(taddr + c0 + cb, a0);
-    if (NC - cb >= 64) tc::tmem_ld32(taddr + c0 + cb + 32, a1);
-    tc::tmem_wait_ld();
+  for (int j = 0; j < 16; ++j) o[j] = leaky_pack(a0[2 * j], a0[2 * j + 1]);
 #pragma unroll
-    for (int q = 0; q < 32; q += 8) leaky_store8(a0 + q, rowp + ((c0 + cb + q) >> 3) * (kTileM * 16));
-    if (NC - cb >= 64) {
-#pragma unroll
-      for (int q = 0; q < 32; q += 8) leaky_store8(a1 + q, rowp + ((c0 + cb + 32 + q) >> 3) * (kTileM * 16));
-    }
-  }
+  for (int j = 0; j < 16; ++j) o[16 + j] = leaky_pack(a1[2 * j], a1[2 * j + 1]);
+  tc::tmem_st32(tA + c0 / 2, o);
 }
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -375,6 +368,8 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   using Lay = MlpLayout<HID>;
   constexpr int K2 = Lay::kK2;
   constexpr int EW = Lay::kEpiWarps;
+  constexpr int NS = Lay::kXStages;
+  static_assert(HID == 128, "the TS-form MLP kernel is specialised for hidden width 128");
   const DevModel& m = P.m;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t xbytes = static_cast<uint32_t>(kTileM) * m.K1P * 2;
@@ -383,15 +378,14 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   uint8_t* sW2 = sW1 + m.w1_bytes;
   uint8_t* sW3 = sW2 + m.w2_bytes;
   uint8_t* sX = sW3 + ((m.w3_bytes + 1023) & ~1023u);
-  uint8_t* sH = sX + 2 * xstage;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sH + 2 * Lay::kHBytes);
-  uint64_t* w_full = bars;          // 1
-  uint64_t* x_full = bars + 1;      // 2
-  uint64_t* x_empty = bars + 3;     // 2
-  uint64_t* l_done = bars + 5;      // 2
-  uint64_t* h_ready = bars + 7;     // 2
-  uint64_t* acc_free = bars + 9;    // 2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + NS * xstage);
+  uint64_t* w_full = bars;                // 1
+  uint64_t* x_full = bars + 1;            // NS
+  uint64_t* x_empty = x_full + NS;        // NS
+  uint64_t* l_done = x_empty + NS;        // 2
+  uint64_t* h_ready = l_done + 2;         // 2
+  uint64_t* acc_free = h_ready + 2;       // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
 
   const int rows = *P.row_counter;
   const int ntiles = (rows + kTileM - 1) / kTileM;
@@ -404,25 +398,18 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   const int lane = tid & 31;
   if (tid == 0) {
     tc::mbar_init(w_full, 1);
+    for (int s = 0; s < NS; ++s) {
+      tc::mbar_init(x_full + s, 1);
+      tc::mbar_init(x_empty + s, 1);
+    }
     for (int g = 0; g < 2; ++g) {
-      tc::mbar_init(x_full + g, 1);
-      tc::mbar_init(x_empty + g, 1);
       tc::mbar_init(l_done + g, 1);
       tc::mbar_init(h_ready + g, EW);   // one arrival per epilogue warp
       tc::mbar_init(acc_free + g, EW);
     }
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * HID);
-  if (warp >= 2 && ((warp - 2) % EW) < 4) {  // bias block of both hidden buffers
-    const int row = 32 * (warp & 3) + lane;
-    const int g = (warp - 2) / EW;
-    const uint32_t hs = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(m.act_scale)));
-    uint8_t* h = sH + g * Lay::kHBytes;
-    *reinterpret_cast<uint4*>(h + canon_offset(row, HID, kTileM)) = make_uint4(hs, 0u, 0u, 0u);
-    *reinterpret_cast<uint4*>(h + canon_offset(row, HID + 8, kTileM)) = make_uint4(0u, 0u, 0u, 0u);
-  }
-  tc::fence_proxy_async_smem();
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * Lay::kGroupCols);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -435,14 +422,12 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       tc::bulk_g2s(sW1, m.w_canon, m.w1_bytes, w_full);
       tc::bulk_g2s(sW2, m.w_canon + m.w1_bytes, m.w2_bytes, w_full);
       tc::bulk_g2s(sW3, m.w_canon + m.w1_bytes + m.w2_bytes, m.w3_bytes, w_full);
-      // X tiles are read once from HBM: keep kPrefetch tiles ahead in flight
-      // as L2 prefetches so the 2-stage SMEM ring is refilled from L2.
-      constexpr int kPrefetch = 6;
+      constexpr int kPrefetch = 8;
       for (int i = 0; i < kPrefetch && i < my_tiles; ++i)
         tc::bulk_prefetch_l2(P.X + static_cast<int64_t>(blockIdx.x + i * gridDim.x) * P.tile_bytes, xbytes);
       for (int i = 0; i < my_tiles; ++i) {
         const int tile = blockIdx.x + i * gridDim.x;
-        const int st = i & 1, k = i >> 1;
+        const int st = i % NS, k = i / NS;
         if (i + kPrefetch < my_tiles)
           tc::bulk_prefetch_l2(P.X + static_cast<int64_t>(tile + kPrefetch * gridDim.x) * P.tile_bytes, xbytes);
         if (k > 0) tc::mbar_wait(x_empty + st, (k - 1) & 1);
@@ -455,19 +440,10 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     if (lane == 0) {
       tc::mbar_wait(w_full, 0);
       const uint32_t sW1_a = tc::smem_addr(sW1), sW2_a = tc::smem_addr(sW2), sW3_a = tc::smem_addr(sW3);
+      const uint32_t sX_a = tc::smem_addr(sX);
       constexpr uint32_t kIdescH = tc::idesc_f16_f32(kTileM, HID);
       const uint32_t idesc3 = tc::idesc_f16_f32(kTileM, m.N3);
       constexpr uint32_t a_lbo = kTileM * 16;
-      auto layer = [&](uint32_t a_base, int ksteps, uint32_t b_base, uint32_t b_rows, uint32_t idesc,
-                       uint32_t d) {
-        tc::tc_fence_after();
-        for (int ks = 0; ks < ksteps; ++ks) {
-          const uint64_t ad = tc::smem_desc(a_base + ks * 2 * a_lbo, a_lbo, 128);
-          const uint64_t bd = tc::smem_desc(b_base + ks * 2 * b_rows * 16, b_rows * 16, 128);
-          tc::mma_f16_ss(d, ad, bd, idesc, ks > 0 ? 1u : 0u);
-        }
-      };
-      // per group: next tile index i (= g + 2k), next layer, barrier phases
       int gi[2] = {0, 1}, gl[2] = {0, 0};
       uint32_t hc[2] = {0, 0};
       while (gi[0] < my_tiles || gi[1] < my_tiles) {
@@ -475,27 +451,41 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
         for (int g = 0; g < 2; ++g) {
           const int i = gi[g];
           if (i >= my_tiles) continue;
-          const int k = i >> 1;
+          const uint32_t tD = tmem + g * Lay::kGroupCols;
+          const uint32_t tA = tD + Lay::kACol;
           if (gl[g] == 0) {
-            if (!mbar_test(x_full + g, k & 1)) continue;
-            if (k > 0 && !mbar_test(acc_free + g, (k - 1) & 1)) continue;
-            layer(tc::smem_addr(sX + g * xstage), m.K1P / 16, sW1_a, HID, kIdescH, tmem + g * HID);
-            tc::mma_commit(x_empty + g);
-            tc::mma_commit(l_done + g);
+            const int st = i % NS, kx = i / NS, ka = i >> 1;
+            if (!mbar_test(x_full + st, kx & 1)) continue;
+            if (ka > 0 && !mbar_test(acc_free + g, (ka - 1) & 1)) continue;
+            tc::tc_fence_after();
+            const uint32_t a_base = sX_a + st * xstage;
+            for (int ks = 0; ks < m.K1P / 16; ++ks) {  // L1: A = X (SMEM)
+              const uint64_t ad = tc::smem_desc(a_base + ks * 2 * a_lbo, a_lbo, 128);
+              const uint64_t bd = tc::smem_desc(sW1_a + ks * 2 * HID * 16, HID * 16, 128);
+              tc::mma_f16_ss(tD, ad, bd, kIdescH, ks > 0 ? 1u : 0u);
+            }
+            tc::mma_commit(x_empty + st);
             gl[g] = 1;
           } else {
             if (!mbar_test(h_ready + g, hc[g] & 1)) continue;
             ++hc[g];
-            if (gl[g] == 1) {
-              layer(tc::smem_addr(sH + g * Lay::kHBytes), K2 / 16, sW2_a, HID, kIdescH, tmem + g * HID);
+            tc::tc_fence_after();
+            if (gl[g] == 1) {  // L2: A = h1 (TMEM), K = HID + bias block
+              for (int ks = 0; ks < K2 / 16; ++ks) {
+                const uint64_t bd = tc::smem_desc(sW2_a + ks * 2 * HID * 16, HID * 16, 128);
+                tc::mma_f16_ts(tD, tA + ks * 8, bd, kIdescH, ks > 0 ? 1u : 0u);
+              }
               gl[g] = 2;
-            } else {
-              layer(tc::smem_addr(sH + g * Lay::kHBytes), HID / 16, sW3_a, m.N3, idesc3, tmem + g * HID);
+            } else {           // L3: A = h2 (TMEM), K = HID, N = 16
+              for (int ks = 0; ks < HID / 16; ++ks) {
+                const uint64_t bd = tc::smem_desc(sW3_a + ks * 2 * m.N3 * 16, m.N3 * 16, 128);
+                tc::mma_f16_ts(tD, tA + ks * 8, bd, idesc3, ks > 0 ? 1u : 0u);
+              }
               gl[g] = 0;
               gi[g] += 2;
             }
-            tc::mma_commit(l_done + g);
           }
+          tc::mma_commit(l_done + g);
         }
       }
     }
@@ -505,8 +495,15 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     const int e = (warp - 2) % EW;
     const int half = e / 4;  // column half; warps e and e+4 share a lane quadrant
     const int row = 32 * (warp & 3) + lane;
-    const uint32_t taddr = tmem + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + g * HID;
-    uint8_t* h = sH + g * Lay::kHBytes;
+    const uint32_t lanes = static_cast<uint32_t>(32 * (warp & 3)) << 16;
+    const uint32_t tD = tmem + lanes + g * Lay::kGroupCols;
+    const uint32_t tA = tD + Lay::kACol;
+    if (half == 0) {  // bias block of A_h: K = HID holds act_scale, HID+1..K2-1 zero
+      const uint32_t hs = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(m.act_scale)));
+      const uint32_t blk[8] = {hs, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      tc::tmem_st8(tA + HID / 2, blk);
+      tc::tmem_wait_st();
+    }
     uint32_t lcount = 0;
     for (int i = g; i < my_tiles; i += 2) {
       const int tile = blockIdx.x + i * gridDim.x;
@@ -518,11 +515,11 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
         mb = __ldg(mp + 1);
       }
 #pragma unroll 1
-      for (int layer = 0; layer < 2; ++layer) {  // h1, h2
+      for (int layer = 0; layer < 2; ++layer) {  // h1, h2 -> A_h
         tc::mbar_wait(l_done + g, lcount++ & 1);
         tc::tc_fence_after();
-        epi_hidden<HID / 2>(taddr, h, row, half * (HID / 2));
-        tc::fence_proxy_async_smem();
+        epi_hidden64(tD, tA, half * 64);
+        tc::tmem_wait_st();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(h_ready + g);
@@ -533,7 +530,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       float z[16];
       if (half == 0) {
         uint32_t acc[16];
-        tc::tmem_ld16(taddr, acc);
+        tc::tmem_ld16(tD, acc);
         tc::tmem_wait_ld();
 #pragma unroll
         for (int q = 0; q < 16; ++q) z[q] = __fadd_rn(__fmul_rn(__uint_as_float(acc[q]), m.inv_act_scale), m.b3[q]);
@@ -551,7 +548,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   __syncthreads();
   if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 2 * HID);
+    tc::tmem_dealloc(tmem, 2 * Lay::kGroupCols);
   }
 }
 
@@ -736,22 +733,35 @@ size_t trace_smem_bytes(const DevModel& m) {
 }
 
 size_t mlp_smem_bytes(const DevModel& m) {
-  const size_t h = static_cast<size_t>(kTileM) * (m.hidden + 16) * 2;
   const size_t x = (static_cast<size_t>(kTileM) * m.K1P * 2 + 1023) & ~size_t(1023);
-  return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + 2 * x + 2 * h + 128;
+  return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + MlpLayout<128>::kXStages * x + 256;
 }
+
+// Per-(kernel, device, smem size) launch configuration, computed once: the
+// attribute and occupancy queries cost microseconds of host time per call.
+struct LaunchCfg {
+  int dev = -1;
+  size_t smem = 0;
+  int sms = 148, per_sm = 1;
+};
 
 template <bool DEBUG, int LS, int FS, bool POW2, int VS>
 static cudaError_t launch_trace_t(const TraceParams& p, cudaStream_t st) {
   auto kern = trace_encode_kernel<DEBUG, LS, FS, POW2, VS>;
   const size_t smem = trace_smem_bytes(p.m);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 148, per_sm = 1;
+  thread_local LaunchCfg cfg;
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem);
+  if (cfg.dev != dev || cfg.smem != smem) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    cudaDeviceGetAttribute(&cfg.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.per_sm, kern, 128, smem);
+    cfg.dev = dev;
+    cfg.smem = smem;
+  }
+  const int sms = cfg.sms, per_sm = cfg.per_sm;
   const int64_t nbatch = (p.n + 127) / 128;
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nbatch, static_cast<int64_t>(sms) * std::max(per_sm, 1)));
   kern<<<grid, 128, smem, st>>>(p);
@@ -770,13 +780,19 @@ cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStrea
   if (max_tiles <= 0) return cudaSuccess;
   const size_t smem = mlp_smem_bytes(p.m);
   const unsigned grid = static_cast<unsigned>(std::min(max_tiles, num_sms));
-  if (p.m.hidden == 128) {
-    cudaFuncSetAttribute(mlp_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    mlp_tc_kernel<128><<<grid, MlpLayout<128>::kThreads, smem, st>>>(p);
-  } else {
-    cudaFuncSetAttribute(mlp_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    mlp_tc_kernel<64><<<grid, MlpLayout<64>::kThreads, smem, st>>>(p);
+  thread_local LaunchCfg cfg[2];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (p.m.hidden != 128) return cudaErrorNotSupported;
+  LaunchCfg& c = cfg[1];
+  if (c.dev != dev || c.smem != smem) {
+    cudaError_t e =
+        cudaFuncSetAttribute(mlp_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    c.dev = dev;
+    c.smem = smem;
   }
+  mlp_tc_kernel<128><<<grid, MlpLayout<128>::kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -81,17 +81,16 @@ int main() {
   uint8_t* g;
   cudaMalloc(&g, size_t(148) * 64 * 28672);
   cudaMemset(g, 0, size_t(148) * 64 * 28672);
-  for (int v : {7, 7 | 32}) {
+  for (int tiles : {256, 10240}) for (int v : {7}) {
     for (int rep = 0; rep < 2; ++rep) {
-      const int tiles = 256;
       bench<<<148, 128, smem>>>(v, tiles, g, d);
       cudaError_t e = cudaDeviceSynchronize();
       unsigned long long h[148];
       cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
       double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
       const int mmas = 16 + ((v & 4) ? 8 : 0);
-      if (rep) printf("variant %d (concurrent TMA=%d): %.0f cycles/tile, %.1f per MMA [%s]\n", v,
-                      (v >> 5) & 1, avg / tiles, avg / tiles / mmas, cudaGetErrorString(e));
+      if (rep) printf("tiles/CTA %d: %.0f cycles/tile, %.1f per MMA [%s]\n", tiles, avg / tiles,
+                      avg / tiles / mmas, cudaGetErrorString(e));
     }
   }
   return 0;
