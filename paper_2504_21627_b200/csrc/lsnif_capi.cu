@@ -141,7 +141,13 @@ struct HostStaging {
 };
 
 constexpr int64_t kChunk = int64_t(1) << 21;      // rays per trace/MLP launch pair
-constexpr int64_t kHostChunk = int64_t(1) << 18;  // rays per host staging step
+constexpr int64_t kHostChunk = int64_t(1) << 17;  // rays per host staging step (LSNIF_HOST_CHUNK overrides)
+
+int64_t host_chunk() {
+  const char* e = std::getenv("LSNIF_HOST_CHUNK");
+  const long long v = e ? std::atoll(e) : 0;
+  return v >= 1024 ? static_cast<int64_t>(v) : kHostChunk;
+}
 constexpr size_t kMaxChunks = 4096;                // row counters per query (2^31 rays)
 // counter block, zeroed by one memset per query: 4 x u64 stats | u32 row
 // counter per chunk | u64 batch counter per chunk
@@ -423,6 +429,17 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
     if (mats.empty()) mats.push_back(lsnif_material{{0.7f, 0.7f, 0.7f}, 0u, 0.5f});
     m.materials = M.upload<lsnif_material>(mats.data(), mats.size() * sizeof(lsnif_material));
     m.n_materials = static_cast<int>(mats.size());
+  }
+
+  {  // constant heads of the all-zero input (rays with a pair but no point)
+    lsnif_hit zh{};
+    ck(lsnif_dev::compute_zero_hit(m, &zh), "zero_hit_kernel");
+    m.zero_lt = zh.t_world;
+    for (int a = 0; a < 3; ++a) {
+      m.zero_normal[a] = zh.normal[a];
+      m.zero_albedo[a] = zh.albedo[a];
+    }
+    m.zero_flags = zh.flags_material & ~static_cast<uint32_t>(LSNIF_HIT_PAIR | LSNIF_HIT_ACCEPTED);
   }
 
   M.info.voxel_res = V;
@@ -757,12 +774,13 @@ lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_
     std::lock_guard<std::mutex> lock(model->staging_mu);
     if (!model->staging) {
       auto s = std::make_unique<HostStaging>();
+      const int64_t cap = host_chunk();
       for (int i = 0; i < kSlots; ++i) {
         ck(cudaStreamCreateWithFlags(&s->streams[i], cudaStreamNonBlocking), "cudaStreamCreate");
-        ck(cudaMalloc(&s->d_rays[i], kHostChunk * sizeof(lsnif_ray)), "cudaMalloc(staging)");
-        ck(cudaMalloc(&s->d_hits[i], kHostChunk * sizeof(lsnif_hit)), "cudaMalloc(staging)");
+        ck(cudaMalloc(&s->d_rays[i], cap * sizeof(lsnif_ray)), "cudaMalloc(staging)");
+        ck(cudaMalloc(&s->d_hits[i], cap * sizeof(lsnif_hit)), "cudaMalloc(staging)");
       }
-      s->cap = kHostChunk;
+      s->cap = cap;
       model->staging = std::move(s);
     }
     HostStaging& S = *model->staging;

@@ -48,6 +48,11 @@ struct DevModel {
   int n_materials;
   float z_zero[32];                    // logits of the all-zero input (rays without points)
   float b3[16];                        // output bias, added in fp32 by the decode epilogue
+  // decode_hit of z_zero with enter = 0, exit = 1 (computed on the device at
+  // load): rays with a pair but no point differ only in t_world and accept
+  float zero_lt;                       // sigmoid(z_zero[1])
+  float zero_normal[3], zero_albedo[3];
+  uint32_t zero_flags;                 // OCCLUDED bit | material << shift
 };
 
 // Row bookkeeping for rays that go through the MLP.
@@ -462,6 +467,27 @@ __device__ __forceinline__ void decode_hit(const float* z, int n_mat, float occ_
   }
   h.flags_material = flags | (static_cast<uint32_t>(arg) << LSNIF_HIT_MATERIAL_SHIFT);
   h.t_world = tw;
+}
+
+// decode_hit(m.z_zero, ...) for a pair without boundary points (the all-zero
+// MLP input): the constant heads come from the load-time decode, only
+// t_world = enter + lt (exit - enter) and the accept rule depend on the ray.
+__device__ __forceinline__ void decode_zero(const DevModel& m, float enter, float exit, float t_min,
+                                            float t_max, int mode, lsnif_hit& h) {
+  const float tw = __fadd_rn(enter, __fmul_rn(m.zero_lt, __fsub_rn(exit, enter)));
+  uint32_t flags = m.zero_flags | LSNIF_HIT_PAIR;
+  if (flags & LSNIF_HIT_OCCLUDED) {
+    const bool accept = (mode == LSNIF_QUERY_CLOSEST) ? !(tw >= t_max || tw < t_min)
+                                                      : (tw >= t_min && tw <= t_max);
+    if (accept) flags |= LSNIF_HIT_ACCEPTED;
+  }
+  h.flags_material = flags;
+  h.t_world = tw;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    h.normal[a] = m.zero_normal[a];
+    h.albedo[a] = m.zero_albedo[a];
+  }
 }
 
 __device__ __forceinline__ void store_hit(lsnif_hit* dst, const lsnif_hit& h) {

@@ -51,6 +51,7 @@ struct InstanceParams {
 };
 
 size_t trace_smem_bytes(const DevModel& m);
+cudaError_t compute_zero_hit(const DevModel& m, lsnif_hit* host_out);  // decode of z_zero, enter 0, exit 1
 cudaError_t launch_scene_init(const lsnif_ray* rays, int64_t n, lsnif_scene_hit* out, cudaStream_t st);
 cudaError_t launch_broad_phase(const DevModel& m, const InstanceParams& ip, const lsnif_ray* rays, int64_t n,
                                lsnif_ray* orays, int32_t* slots, int32_t* count, cudaStream_t st);

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
         store_hit(P.out + ray_idx, h);
       } else if (pair && count == 0) {
         lsnif_hit h;
-        decode_hit(m.z_zero, m.n_mat, m.occ_threshold, enter, exit, t_min, t_max, P.mode, true, h);
+        decode_zero(m, enter, exit, t_min, t_max, P.mode, h);
         store_hit(P.out + ray_idx, h);
       }
     } else if (live) {
@@ -726,6 +726,25 @@ __global__ void __launch_bounds__(128) infer_f32_kernel(const DevModel m, const 
 }
 
 // ================================================================ launch
+
+__global__ void zero_hit_kernel(const DevModel m, lsnif_hit* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    lsnif_hit h;
+    decode_hit(m.z_zero, m.n_mat, m.occ_threshold, 0.0f, 1.0f, 0.0f, 0.0f, LSNIF_QUERY_CLOSEST, false, h);
+    *out = h;
+  }
+}
+
+cudaError_t compute_zero_hit(const DevModel& m, lsnif_hit* host_out) {
+  lsnif_hit* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(lsnif_hit));
+  if (e != cudaSuccess) return e;
+  zero_hit_kernel<<<1, 32>>>(m, d);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(host_out, d, sizeof(lsnif_hit), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e;
+}
 
 size_t trace_smem_bytes(const DevModel& m) {
   const size_t occ_words = static_cast<size_t>(m.stop_words);

@@ -21,7 +21,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblsnif_gpu.so")
+LIB_PATH = os.environ.get("LSNIF_LIB") or os.path.join(HERE, "liblsnif_gpu.so")  # override: A/B builds
 
 RAY_DTYPE = np.dtype([("o", "<f4", 3), ("d", "<f4", 3), ("t_min", "<f4"), ("t_max", "<f4")])
 HIT_DTYPE = np.dtype([("flags_material", "<u4"), ("t_world", "<f4"), ("normal", "<f4", 3),
