@@ -1,7 +1,7 @@
 # Builds liblsnif_gpu.so (sm_100a) in-tree, and the CPU oracle (test infra).
 NVCC ?= /usr/local/cuda/bin/nvcc
 PKG := paper_2504_21627_b200
-SRC := $(PKG)/csrc/lsnif_kernels.cu $(PKG)/csrc/lsnif_capi.cu
+SRC := $(PKG)/csrc/lsnif_kernels.cu $(PKG)/csrc/lsnif_capi.cu $(PKG)/csrc/lsnif_render.cu
 HDR := $(wildcard $(PKG)/csrc/*.cuh $(PKG)/csrc/*.hpp) include/lsnif_gpu.h
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
            -Xcompiler -fPIC -Xcompiler -ffp-contract=off -Xptxas -v \

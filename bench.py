@@ -47,6 +47,10 @@ WORKLOADS = {
     "c4": "C4 (configs[3]): 8 LSNIF instances (teapot x3, sphere x2, torus x2, box; "
           "per-object hash grids and MLP weights, seeds 0-3) on a 4x2 grid, 1920x1080 camera "
           "rays, brute-force broad phase + per-object narrow phase + closest-hit merge, per GPU",
+    "render": "F3 (SURVEY §8(f)): wavefront path tracer over a 4-instance LSNIF scene (teapot with "
+              "glossy lid, glossy sphere, box, torus; point + sphere light, environment), "
+              "1280x720 x 4 spp, 4 bounces, PrimaryMode::lsnif; rays = intersect_scene + "
+              "occluded_batch queries issued by the renderer",
     "c5": "C5 (configs[4]): teapot LSNIF, 3840x2160 x 16 spp incoherent rays (132,710,400, "
           "keyed by (pixel, sample)), closest-hit, row bands tile-sharded across the GPUs with "
           "an NCCL result gather to rank 0 inside the step (strong scaling)",
@@ -303,6 +307,112 @@ def run_c4(args, rank, world, dev, gpu, max_over_ranks):
         print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------- F3 renderer
+
+RENDER_CFG = dict(width=1280, height=720, spp=4, max_bounces=4, seed=1, neural_eps_scale=1e-3)
+
+
+def render_scene_paths(tmpdir: str):
+    from paper_2504_21627_b200 import workloads as W
+    gold = os.path.join(ROOT, "tests", "golden")
+    paths = [os.path.join(gold, n + ".lsnif") for n in W.RENDER_MODELS]
+    paths[0] = W.glossy_copy(paths[0], os.path.join(tmpdir, "teapot_glossy.lsnif"), 1, 0.3)
+    paths[1] = W.glossy_copy(paths[1], os.path.join(tmpdir, "sphere_glossy.lsnif"), 0, 0.2)
+    return paths
+
+
+def run_render(args, rank, world, dev, gpu, max_over_ranks):
+    """One step = one full render (camera rays, 4 bounces, NEE shadow rays)
+    through lsnif_render; value = renderer ray queries per second."""
+    import tempfile
+    import torch
+    from paper_2504_21627_b200 import lsnif, workloads as W
+    tmp = tempfile.mkdtemp(prefix="lsnif_render_")
+    paths = render_scene_paths(tmp)
+    models = [lsnif.GpuModel(p, gpu) for p in paths]
+    w2o = W.render_world_to_object()
+    scene = lsnif.GpuScene([(models[i], w2o[i]) for i in range(len(models))])
+    diag = W.world_diag_from_frames([m.aabb for m in models])
+    cfg = dict(RENDER_CFG, seed=RENDER_CFG["seed"] + rank)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    st = {}
+    for _ in range(args.warmup):
+        img = scene.render(W.RENDER_CAMERA, W.RENDER_LIGHTS, W.RENDER_ENV, cfg, diag, stats=st)
+    torch.cuda.synchronize()
+    for m in models:
+        m.profile_read(reset=True, stream="all")
+        m.profile_enable(True)
+    clocks = ClockSampler(gpu)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    clocks.start()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record()
+        img = scene.render(W.RENDER_CAMERA, W.RENDER_LIGHTS, W.RENDER_ENV, cfg, diag, stats=st)
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    clocks.stop()
+    profs = []
+    for m in models:
+        m.profile_enable(False)
+        profs.append(m.profile_read(reset=True, stream="all"))
+    elapsed_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
+    rays = st["closest_rays"] + st["shadow_rays"]
+    value = world * rays * args.steps / (elapsed_ms / 1e3)
+    # e2e: the same render through the public API + the image read back to the host
+    host = torch.empty(img.shape, dtype=torch.float32).pin_memory()
+    t0 = time.perf_counter()
+    e2e_steps = max(2, min(args.steps, 5))
+    for _ in range(e2e_steps):
+        img = scene.render(W.RENDER_CAMERA, W.RENDER_LIGHTS, W.RENDER_ENV, cfg, diag)
+        host.copy_(img)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    if rank != 0:
+        return
+    tr = sum(p["trace_ms"] for p in profs) / args.steps
+    ml = sum(p["mlp_ms"] for p in profs) / args.steps
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32 traversal/encode/shading + f16xf16->f32 tcgen05 MLP", "data": "synthetic",
+            "config": {"workload": WORKLOADS["render"], "render": cfg,
+                       "l2": "flushed between timed steps (256 MiB write outside the events)",
+                       "parallelism": f"dp{world} (one frame per GPU)"},
+            "workload_stats": {k: int(v) for k, v in st.items()},
+            "kernels": {"trace_encode_kernel": {"ms_per_step": tr},
+                        "mlp_tc_kernel": {"ms_per_step": ml}},
+            "e2e": {"value": world * rays * e2e_steps / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": int(img.numel() * 4), "steps": e2e_steps,
+                    "api": "lsnif_render + image D2H (inputs are the scene / camera description)"},
+            "gpu_launches": sum(int(p["launches"]) for p in profs),
+            "clocks": clocks.summary()}
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            O = cpu_oracle(True)
+            om = [O.OracleModel.load(p, fast=True) for p in paths]
+            small = dict(cfg, width=320, height=180)
+            ost = {}
+            O.render(om, w2o, W.RENDER_CAMERA, W.RENDER_LIGHTS, W.RENDER_ENV, dict(small, height=18),
+                     diag, workers=0)  # warm-up
+            t0 = time.perf_counter()
+            O.render(om, w2o, W.RENDER_CAMERA, W.RENDER_LIGHTS, W.RENDER_ENV, small, diag, workers=0,
+                     stats=ost)
+            dt = time.perf_counter() - t0
+            cores = int(O.lib(True).oracle_hardware_concurrency())
+            line["cpu_baseline"] = {
+                "value": (ost["closest_rays"] + ost["shadow_rays"]) / dt, "unit": UNIT, "cores": cores,
+                "kind": "port",
+                "sample": f"the same scene/config at 320x180 ({ost['closest_rays']} + "
+                          f"{ost['shadow_rays']} rays, {dt:.1f} s, oracle render restatement)"}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line), flush=True)
+
+
 # --------------------------------------------------------------------- ours
 
 def main():
@@ -335,8 +445,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    if args.workload == "c4":
-        run_c4(args, rank, world, dev, gpu, max_over_ranks)
+    if args.workload in ("c4", "render"):
+        (run_c4 if args.workload == "c4" else run_render)(args, rank, world, dev, gpu, max_over_ranks)
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()

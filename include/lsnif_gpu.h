@@ -206,6 +206,67 @@ lsnif_status lsnif_scene_destroy(lsnif_scene scene);
 lsnif_status lsnif_scene_query(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n, int mode,
                                lsnif_scene_hit* d_hits, void* stream);
 
+/* ---- wavefront path tracer ----
+ * lsnif::Camera (scene.hpp:12-17), lsnif::Light (scene.hpp:19-26; point and
+ * sphere lights — environment lights are summed into `environment` as
+ * PreparedScene::prepare does, renderer.cpp:46-51) and the RenderConfig
+ * fields the renderer reads (renderer.hpp:14-28). */
+typedef struct lsnif_camera {
+  float position[3];
+  float look_at[3];
+  float up[3];
+  float vfov_deg;
+} lsnif_camera;
+
+enum { LSNIF_LIGHT_POINT = 0, LSNIF_LIGHT_SPHERE = 1 };
+typedef struct lsnif_light {
+  uint32_t type;
+  float position[3];
+  float radius;
+  float radiance[3];
+} lsnif_light;
+
+typedef struct lsnif_render_config {
+  int32_t width, height, spp, max_bounces;
+  uint64_t seed;
+  float neural_eps_scale; /* respawn offset for neural hits, x object world diagonal */
+  int32_t max_paths_in_flight; /* 0 = library default; bounds device memory per wave */
+} lsnif_render_config;
+
+/* Ray counts of one lsnif_render call (optional output). */
+typedef struct lsnif_render_stats {
+  int64_t paths;          /* width * height * spp */
+  int64_t closest_rays;   /* intersect_scene queries: camera + bounce rays */
+  int64_t shadow_slots;   /* occluded_batch queries (fixed per-path slots, incl. empty) */
+  int64_t shadow_rays;    /* filled shadow slots */
+  int32_t waves;
+  int32_t max_depth_reached;
+} lsnif_render_stats;
+
+/* Replaces render() (renderer.cpp:453-542) with PrimaryMode::lsnif for a
+ * scene whose objects are all LSNIF instances: per path the reference's
+ * mt19937 stream (seed_stream(seed, pixel, sample)), camera_ray, and per
+ * bounce intersect_scene (lsnif_scene_query, CLOSEST), shade_hit (NEE to
+ * every light + BSDF sample, renderer.cpp:378-442) and occluded_batch on the
+ * shadow rays (lsnif_scene_query, ANY); the environment on a miss. Paths are
+ * device resident between bounces (wavefront). `world_diag[i]` is
+ * PreparedObject::world_diag of instance i (renderer.cpp:73-74; the mesh is
+ * not part of the model). d_image: DEVICE float[height][width][3], written
+ * as the spp-average like the reference's Image. At most 227 random draws
+ * per path (2 + (max_bounces+1) * (2 * n_sphere_lights + 2)); larger
+ * configurations return LSNIF_UNSUPPORTED. `stats` may be NULL. Synchronous. */
+lsnif_status lsnif_render(lsnif_scene scene, const float* world_diag, int32_t n_instances,
+                          const lsnif_camera* camera, const lsnif_light* lights, int32_t n_lights,
+                          const float environment[3], const lsnif_render_config* config,
+                          float* d_image, lsnif_render_stats* stats, void* stream);
+
+/* Test probe of the renderer's sampling: for paths [first_path, first_path+n)
+ * (path = pixel * spp + sample) the primary ray (renderer.cpp:347-361) and the
+ * next k uniform draws of the path's stream. DEVICE outputs. */
+lsnif_status lsnif_render_debug_paths(const lsnif_camera* camera, const lsnif_render_config* config,
+                                      int64_t first_path, int64_t n, lsnif_ray* d_rays,
+                                      float* d_uniforms, int32_t k, void* stream);
+
 /* Kernel-level timing of queries (bench / roofline support). When enabled,
  * CUDA events are recorded on the query stream around every kernel launch;
  * lsnif_profile_read synchronises `stream` and returns the summed device

@@ -73,6 +73,8 @@ def _load(path: str) -> C.CDLL:
     f.oracle_trace.argtypes = [_P, _P, C.c_int64] + [_P] * 7
     f.oracle_build_shape_model.argtypes = [C.c_int, C.c_uint64, C.c_char_p]
     f.oracle_scene_query.argtypes = [_P, _P, C.c_int, _P, C.c_int64, C.c_int, _P, C.c_int]
+    f.oracle_render.argtypes = [_P, _P, C.c_int, _P, _P, C.c_int, _P, _P, C.c_int, _P]
+    f.oracle_render_debug_paths.argtypes = [_P, C.c_int64, C.c_int64, _P, _P, C.c_int]
     return lib
 
 
@@ -259,3 +261,58 @@ def voxelize(verts: np.ndarray, faces: np.ndarray, frame, res: int) -> np.ndarra
     out = np.zeros(res ** 3 // 8, np.uint8)
     _check(L.oracle_voxelize(_ptr(v), len(v), _ptr(f), len(f), _ptr(fr), res, _ptr(out)), L)
     return out
+
+
+# ---- path tracer (renderer.cpp:330-542), LSNIF-only scenes, primary = lsnif
+
+def render_setup_array(camera: dict, cfg: dict, environment=(0.0, 0.0, 0.0)) -> np.ndarray:
+    """Packs RenderConfig + camera + environment into the oracle's float block."""
+    a = np.zeros(20, np.float32)
+    u = a.view(np.uint32)
+    u[0], u[1], u[2], u[3] = cfg["width"], cfg["height"], cfg["spp"], cfg["max_bounces"]
+    seed = int(cfg.get("seed", 0))
+    u[4], u[5] = seed & 0xFFFFFFFF, seed >> 32
+    a[6] = cfg.get("neural_eps_scale", 1e-3)
+    a[7:10], a[10:13], a[13:16] = camera["position"], camera["look_at"], camera["up"]
+    a[16] = camera["vfov_deg"]
+    a[17:20] = environment
+    return a
+
+
+def lights_array(lights) -> np.ndarray:
+    a = np.zeros((max(len(lights), 1), 8), np.float32)
+    for i, L in enumerate(lights):
+        a[i, 0:1].view(np.uint32)[0] = 1 if L["type"] == "sphere" else 0
+        a[i, 1:4] = L["position"]
+        a[i, 4] = L.get("radius", 0.0)
+        a[i, 5:8] = L["radiance"]
+    return a
+
+
+def render(models, w2o, camera: dict, lights, environment, cfg: dict, world_diag,
+           workers: int = 0, stats: dict | None = None) -> np.ndarray:
+    """render() for instances (models[k], w2o[k]); returns (H, W, 3) float32.
+    `stats` receives the intersect_scene / occluded_batch ray counts."""
+    L = models[0].L
+    handles = (C.c_void_p * len(models))(*[m.h for m in models])
+    w = np.ascontiguousarray(np.asarray(w2o, np.float32).reshape(len(models), 12))
+    setup = render_setup_array(camera, cfg, environment)
+    la = lights_array(lights)
+    diag = np.ascontiguousarray(world_diag, np.float32)
+    img = np.zeros((cfg["height"], cfg["width"], 3), np.float32)
+    st = np.zeros(2, np.int64)
+    _check(L.oracle_render(C.cast(handles, C.c_void_p), _ptr(w), len(models), _ptr(setup), _ptr(la),
+                           len(lights), _ptr(diag), _ptr(img), workers, _ptr(st)), L)
+    if stats is not None:
+        stats.update(closest_rays=int(st[0]), shadow_rays=int(st[1]))
+    return img
+
+
+def render_debug_paths(camera: dict, cfg: dict, first: int, n: int, k: int):
+    """Primary rays and the next k uniforms of paths [first, first + n)."""
+    L = lib()
+    setup = render_setup_array(camera, cfg)
+    rays = np.zeros(n, RAY_DTYPE)
+    u = np.zeros((n, max(k, 1)), np.float32)
+    _check(L.oracle_render_debug_paths(_ptr(setup), first, n, _ptr(rays), _ptr(u), k), L)
+    return rays, u[:, :k]

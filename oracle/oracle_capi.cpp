@@ -3,6 +3,7 @@
 // (ctypes). Errors: functions return a negative status and set a
 // thread-local message readable with oracle_last_error().
 #include "lsnif_oracle.hpp"
+#include "lsnif_render_oracle.hpp"
 
 #include <chrono>
 #include <cmath>
@@ -365,6 +366,46 @@ int oracle_scene_query(void** models, const float* w2o, int n_inst, const Ray* r
     }
     scene_query(inst.data(), n_inst, rays, n, mode, out, workers);
   });
+}
+
+// setup layout (floats): width, height, spp, max_bounces, seed_lo, seed_hi (as
+// u32 bit patterns), eps, camera[10], environment[3]; lights: 8 floats each
+// (type as u32 bits, position, radius, radiance).
+static RenderSetup unpack_setup(const float* sp, const float* lights, int n_lights, const float* diag, int n_inst) {
+  RenderSetup S;
+  const uint32_t* u = reinterpret_cast<const uint32_t*>(sp);
+  S.width = static_cast<int>(u[0]);
+  S.height = static_cast<int>(u[1]);
+  S.spp = static_cast<int>(u[2]);
+  S.max_bounces = static_cast<int>(u[3]);
+  S.seed = static_cast<uint64_t>(u[4]) | (static_cast<uint64_t>(u[5]) << 32);
+  S.neural_eps_scale = sp[6];
+  std::memcpy(&S.camera, sp + 7, sizeof(RCamera));
+  for (int a = 0; a < 3; ++a) S.environment[a] = sp[17 + a];
+  for (int i = 0; i < n_lights; ++i) {
+    RLight L;
+    std::memcpy(&L, lights + 8 * i, sizeof(RLight));
+    S.lights.push_back(L);
+  }
+  S.world_diag.assign(diag, diag + n_inst);
+  return S;
+}
+
+int oracle_render(void** models, const float* w2o, int n_inst, const float* setup, const float* lights,
+                  int n_lights, const float* world_diag, float* image, int workers, int64_t* stats) {
+  return guarded([&] {
+    std::vector<Instance> inst(static_cast<size_t>(n_inst));
+    for (int k = 0; k < n_inst; ++k) {
+      inst[static_cast<size_t>(k)].model = static_cast<Model*>(models[k]);
+      std::memcpy(inst[static_cast<size_t>(k)].w2o, w2o + 12 * k, 48);
+    }
+    render(unpack_setup(setup, lights, n_lights, world_diag, n_inst), inst.data(), n_inst, image, workers,
+           stats);
+  });
+}
+
+int oracle_render_debug_paths(const float* setup, int64_t first, int64_t n, Ray* rays, float* u, int k) {
+  return guarded([&] { render_debug_paths(unpack_setup(setup, nullptr, 0, nullptr, 0), first, n, rays, u, k); });
 }
 
 }  // extern "C"

@@ -24,16 +24,9 @@ namespace {
 
 thread_local std::string g_err;
 
-struct ApiError {
-  lsnif_status st;
-  std::string msg;
-};
-
-[[noreturn]] void fail(lsnif_status st, const std::string& msg) { throw ApiError{st, msg}; }
-
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) fail(LSNIF_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
-}
+using lsnif_api::ApiError;
+using lsnif_api::ck;
+using lsnif_api::fail;
 
 template <typename F>
 lsnif_status guarded(F&& f) {
@@ -646,6 +639,8 @@ struct lsnif_scene_s {
   };
   std::mutex mu;
   std::map<cudaStream_t, std::unique_ptr<Scratch>> scratch;
+  std::mutex render_mu;
+  std::map<cudaStream_t, lsnif_pt::WorkspacePtr> render_ws;  // renderer path state per stream
 
   Scratch& get(cudaStream_t st, int64_t n) {
     std::lock_guard<std::mutex> lock(mu);
@@ -669,6 +664,32 @@ struct lsnif_scene_s {
     return *s;
   }
 };
+
+namespace lsnif_api {
+
+void scene_query_async(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n, const int32_t* d_n, int mode,
+                       lsnif_scene_hit* d_hits, cudaStream_t st) {
+  if (!scene) fail(LSNIF_INVALID_ARGUMENT, "null scene");
+  if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
+  if (mode != LSNIF_QUERY_CLOSEST && mode != LSNIF_QUERY_ANY) fail(LSNIF_INVALID_ARGUMENT, "bad query mode");
+  if (n > 0 && (!d_rays || !d_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
+  if (n > INT32_MAX) fail(LSNIF_INVALID_ARGUMENT, "more than 2^31-1 rays in one call");
+  if (n == 0) return;
+  ck(cudaSetDevice(scene->device), "cudaSetDevice");
+  auto& S = scene->get(st, n);
+  ck(lsnif_dev::launch_scene_init(d_rays, n, d_n, d_hits, st), "scene_init_kernel");
+  for (size_t k = 0; k < scene->inst.size(); ++k) {  // object order (renderer.cpp:175-179)
+    lsnif_model_s& M = *scene->models[k];
+    ck(cudaMemsetAsync(S.count, 0, 4, st), "cudaMemsetAsync");
+    ck(lsnif_dev::launch_broad_phase(M.dm, scene->inst[k], d_rays, n, d_n, S.orays, S.slots, S.count, st),
+       "broad_phase_kernel");
+    run_query(M, S.orays, n, mode, S.hits, st, S.count);
+    ck(lsnif_dev::launch_merge(M.dm, scene->inst[k], d_rays, S.hits, S.slots, S.count, n, mode, d_hits, st),
+       "merge_kernel");
+  }
+}
+
+}  // namespace lsnif_api
 
 extern "C" {
 
@@ -701,31 +722,43 @@ lsnif_status lsnif_scene_destroy(lsnif_scene scene) {
 lsnif_status lsnif_scene_query(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n, int mode,
                                lsnif_scene_hit* d_hits, void* stream) {
   return guarded([&] {
-    if (!scene) fail(LSNIF_INVALID_ARGUMENT, "null scene");
-    if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
-    if (mode != LSNIF_QUERY_CLOSEST && mode != LSNIF_QUERY_ANY) fail(LSNIF_INVALID_ARGUMENT, "bad query mode");
-    if (n > 0 && (!d_rays || !d_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
-    if (n > INT32_MAX) fail(LSNIF_INVALID_ARGUMENT, "more than 2^31-1 rays in one call");
-    if (n == 0) return;
+    lsnif_api::scene_query_async(scene, d_rays, n, nullptr, mode, d_hits, static_cast<cudaStream_t>(stream));
+  });
+}
+
+lsnif_status lsnif_render(lsnif_scene scene, const float* world_diag, int32_t n_instances,
+                          const lsnif_camera* camera, const lsnif_light* lights, int32_t n_lights,
+                          const float environment[3], const lsnif_render_config* config,
+                          float* d_image, lsnif_render_stats* stats, void* stream) {
+  return guarded([&] {
+    if (!scene || !camera || !config) fail(LSNIF_INVALID_ARGUMENT, "null scene, camera or config");
+    if (n_instances != static_cast<int32_t>(scene->inst.size()))
+      fail(LSNIF_INVALID_ARGUMENT, "render: world_diag needs one entry per scene instance");
+    if (n_instances > 0 && !world_diag) fail(LSNIF_INVALID_ARGUMENT, "render: null world_diag");
     ck(cudaSetDevice(scene->device), "cudaSetDevice");
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    auto& S = scene->get(st, n);
-    ck(lsnif_dev::launch_scene_init(d_rays, n, d_hits, st), "scene_init_kernel");
-    for (size_t k = 0; k < scene->inst.size(); ++k) {  // object order (renderer.cpp:175-179)
-      lsnif_model_s& M = *scene->models[k];
-      ck(cudaMemsetAsync(S.count, 0, 4, st), "cudaMemsetAsync");
-      ck(lsnif_dev::launch_broad_phase(M.dm, scene->inst[k], d_rays, n, S.orays, S.slots, S.count, st),
-         "broad_phase_kernel");
-      run_query(M, S.orays, n, mode, S.hits, st, S.count);
-      ck(lsnif_dev::launch_merge(M.dm, scene->inst[k], d_rays, S.hits, S.slots, S.count, n, mode, d_hits, st),
-         "merge_kernel");
+    lsnif_pt::WorkspacePtr* ws = nullptr;
+    {
+      std::lock_guard<std::mutex> lock(scene->render_mu);
+      ws = &scene->render_ws[static_cast<cudaStream_t>(stream)];
     }
+    lsnif_pt::render(*ws, scene, world_diag, n_instances, *camera, lights, n_lights, environment, *config,
+                     d_image, stats, static_cast<cudaStream_t>(stream));
+  });
+}
+
+lsnif_status lsnif_render_debug_paths(const lsnif_camera* camera, const lsnif_render_config* config,
+                                      int64_t first_path, int64_t n, lsnif_ray* d_rays,
+                                      float* d_uniforms, int32_t k, void* stream) {
+  return guarded([&] {
+    if (!camera || !config) fail(LSNIF_INVALID_ARGUMENT, "null camera or config");
+    lsnif_pt::debug_paths(*camera, *config, first_path, n, d_rays, d_uniforms, k,
+                              static_cast<cudaStream_t>(stream));
   });
 }
 
 const char* lsnif_build_info(void) {
   return "liblsnif_gpu sm_100a: trace_encode_kernel + mlp_tc_kernel (tcgen05 kind::f16, TMEM), "
-         "infer_f32_kernel";
+         "infer_f32_kernel; wavefront renderer (camera/shade/shadow_accum/resolve kernels)";
 }
 
 lsnif_status lsnif_model_create(const lsnif_model_desc* desc, int device, lsnif_model* out) {

@@ -5,8 +5,24 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <memory>
+#include <string>
 
 #include "lsnif_device.cuh"
+
+// Error plumbing shared by the C-ABI translation units: entry points throw
+// ApiError and the guarded() wrapper in lsnif_capi.cu turns it into a status
+// plus the thread-local message.
+namespace lsnif_api {
+struct ApiError {
+  lsnif_status st;
+  std::string msg;
+};
+[[noreturn]] inline void fail(lsnif_status st, const std::string& msg) { throw ApiError{st, msg}; }
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(LSNIF_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace lsnif_api
 
 namespace lsnif_dev {
 
@@ -52,9 +68,12 @@ struct InstanceParams {
 
 size_t trace_smem_bytes(const DevModel& m);
 cudaError_t compute_zero_hit(const DevModel& m, lsnif_hit* host_out);  // decode of z_zero, enter 0, exit 1
-cudaError_t launch_scene_init(const lsnif_ray* rays, int64_t n, lsnif_scene_hit* out, cudaStream_t st);
+// n_dev (nullable): device-side ray count, n its upper bound
+cudaError_t launch_scene_init(const lsnif_ray* rays, int64_t n, const int32_t* n_dev, lsnif_scene_hit* out,
+                              cudaStream_t st);
 cudaError_t launch_broad_phase(const DevModel& m, const InstanceParams& ip, const lsnif_ray* rays, int64_t n,
-                               lsnif_ray* orays, int32_t* slots, int32_t* count, cudaStream_t st);
+                               const int32_t* n_dev, lsnif_ray* orays, int32_t* slots, int32_t* count,
+                               cudaStream_t st);
 cudaError_t launch_merge(const DevModel& m, const InstanceParams& ip, const lsnif_ray* rays,
                          const lsnif_hit* hits, const int32_t* slots, const int32_t* count, int64_t n_max,
                          int mode, lsnif_scene_hit* out, cudaStream_t st);
@@ -65,3 +84,24 @@ cudaError_t launch_infer_f32(const DevModel& m, const float* x, int64_t n, const
                              lsnif_hit* out, cudaStream_t st);
 
 }  // namespace lsnif_dev
+
+// Scene query with a device-side ray count (n_max bounds it): no host sync,
+// so a caller can enqueue dependent work (lsnif_capi.cu).
+namespace lsnif_api {
+void scene_query_async(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n_max, const int32_t* d_n, int mode,
+                       lsnif_scene_hit* d_hits, cudaStream_t st);
+}  // namespace lsnif_api
+
+// Wavefront path tracer (lsnif_render.cu), driven by lsnif_render in lsnif_capi.cu.
+namespace lsnif_pt {
+struct Workspace;  // per (scene, stream) path-state buffers, reused across renders
+struct WorkspaceDeleter {
+  void operator()(Workspace* w) const;
+};
+using WorkspacePtr = std::unique_ptr<Workspace, WorkspaceDeleter>;
+void render(WorkspacePtr& ws, lsnif_scene scene, const float* world_diag, int n_instances, const lsnif_camera& camera,
+            const lsnif_light* lights, int n_lights, const float environment[3],
+            const lsnif_render_config& cfg, float* d_image, lsnif_render_stats* stats, cudaStream_t st);
+void debug_paths(const lsnif_camera& camera, const lsnif_render_config& cfg, int64_t first_path,
+                 int64_t n, lsnif_ray* d_rays, float* d_uniforms, int k, cudaStream_t st);
+}  // namespace lsnif_pt

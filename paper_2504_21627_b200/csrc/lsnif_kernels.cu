@@ -555,8 +555,10 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
 // ===================================================== multi-object scenes
 
 // best_t = ray.t_max (no triangle objects, renderer.cpp:275), no hit.
-__global__ void scene_init_kernel(const lsnif_ray* __restrict__ rays, int64_t n, lsnif_scene_hit* out) {
+__global__ void scene_init_kernel(const lsnif_ray* __restrict__ rays, int64_t n, const int32_t* n_dev,
+                                  lsnif_scene_hit* out) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (n_dev) n = min(n, static_cast<int64_t>(*n_dev));
   if (i >= n) return;
   float4* o = reinterpret_cast<float4*>(out + i);
   const float t_max = rays[i].t_max;
@@ -583,8 +585,11 @@ __device__ __forceinline__ void to_object(const float* L, const float p[3], cons
 // Emits the compacted object-space rays (t_max = the pair gate) + slots.
 __global__ void __launch_bounds__(256) broad_phase_kernel(const DevModel m, const InstanceParams ip,
                                                           const lsnif_ray* __restrict__ rays, int64_t n,
+                                                          const int32_t* n_dev,
                                                           lsnif_ray* __restrict__ orays, int32_t* __restrict__ slots,
                                                           int32_t* count) {
+  if (n_dev) n = min(n, static_cast<int64_t>(*n_dev));
+  if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= n) return;  // whole block past the count
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   bool keep = false;
@@ -664,16 +669,19 @@ __global__ void __launch_bounds__(256) merge_kernel(const DevModel m, const Inst
   }
 }
 
-cudaError_t launch_scene_init(const lsnif_ray* rays, int64_t n, lsnif_scene_hit* out, cudaStream_t st) {
+cudaError_t launch_scene_init(const lsnif_ray* rays, int64_t n, const int32_t* n_dev, lsnif_scene_hit* out,
+                              cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  scene_init_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(rays, n, out);
+  scene_init_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(rays, n, n_dev, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_broad_phase(const DevModel& m, const InstanceParams& ip, const lsnif_ray* rays, int64_t n,
-                               lsnif_ray* orays, int32_t* slots, int32_t* count, cudaStream_t st) {
+                               const int32_t* n_dev, lsnif_ray* orays, int32_t* slots, int32_t* count,
+                               cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  broad_phase_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(m, ip, rays, n, orays, slots, count);
+  broad_phase_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(m, ip, rays, n, n_dev, orays, slots,
+                                                                            count);
   return cudaGetLastError();
 }
 

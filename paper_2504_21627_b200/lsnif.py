@@ -85,10 +85,13 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.lsnif_scene_destroy.argtypes = [P]
     lib.lsnif_scene_query.argtypes = [P, P, C.c_int64, C.c_int, P, P]
     lib.lsnif_profile_read.argtypes = [P, P, C.c_int, C.POINTER(Profile)]
+    lib.lsnif_render.argtypes = [P, P, C.c_int32, P, P, C.c_int32, P, P, P, P, P]
+    lib.lsnif_render_debug_paths.argtypes = [P, P, C.c_int64, C.c_int64, P, P, C.c_int32, P]
     for name in ("lsnif_model_load", "lsnif_model_destroy", "lsnif_model_get_info", "lsnif_query",
                  "lsnif_query_host", "lsnif_infer_batch", "lsnif_debug_traverse",
                  "lsnif_last_query_stats", "lsnif_profile_enable", "lsnif_profile_read",
-                 "lsnif_scene_create", "lsnif_scene_destroy", "lsnif_scene_query"):
+                 "lsnif_scene_create", "lsnif_scene_destroy", "lsnif_scene_query", "lsnif_render",
+                 "lsnif_render_debug_paths"):
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -226,6 +229,54 @@ class GpuModel:
         return ((h["flags_material"] & ACCEPTED) != 0).astype(np.int8)
 
 
+class Camera(C.Structure):
+    _fields_ = [("position", C.c_float * 3), ("look_at", C.c_float * 3), ("up", C.c_float * 3),
+                ("vfov_deg", C.c_float)]
+
+
+class Light(C.Structure):
+    _fields_ = [("type", C.c_uint32), ("position", C.c_float * 3), ("radius", C.c_float),
+                ("radiance", C.c_float * 3)]
+
+
+class RenderConfig(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("spp", C.c_int32),
+                ("max_bounces", C.c_int32), ("seed", C.c_uint64), ("neural_eps_scale", C.c_float),
+                ("max_paths_in_flight", C.c_int32)]
+
+
+def _camera(camera: dict) -> Camera:
+    c = Camera()
+    c.position[:], c.look_at[:], c.up[:] = camera["position"], camera["look_at"], camera["up"]
+    c.vfov_deg = camera["vfov_deg"]
+    return c
+
+
+def _config(cfg: dict) -> RenderConfig:
+    r = RenderConfig()
+    r.width, r.height, r.spp, r.max_bounces = cfg["width"], cfg["height"], cfg["spp"], cfg["max_bounces"]
+    r.seed = int(cfg.get("seed", 0))
+    r.neural_eps_scale = cfg.get("neural_eps_scale", 1e-3)
+    r.max_paths_in_flight = int(cfg.get("max_paths_in_flight", 0))
+    return r
+
+
+def render_debug_paths(camera: dict, cfg: dict, first: int, n: int, k: int, device="cuda"):
+    """GPU sampling probe: primary rays (n, 8) and the next k uniforms (n, k)."""
+    torch = _torch()
+    rays = torch.empty((n, 8), dtype=torch.float32, device=device)
+    u = torch.empty((n, max(k, 1)), dtype=torch.float32, device=device)
+    _check(load_library().lsnif_render_debug_paths(C.byref(_camera(camera)), C.byref(_config(cfg)),
+                                                   first, n, rays.data_ptr(), u.data_ptr(), k,
+                                                   _stream_ptr(None)))
+    return rays, u[:, :k]
+
+
+class RenderStats(C.Structure):
+    _fields_ = [("paths", C.c_int64), ("closest_rays", C.c_int64), ("shadow_slots", C.c_int64),
+                ("shadow_rays", C.c_int64), ("waves", C.c_int32), ("max_depth_reached", C.c_int32)]
+
+
 class Instance(C.Structure):
     _fields_ = [("model", C.c_void_p), ("world_to_object", C.c_float * 12)]
 
@@ -255,6 +306,31 @@ class GpuScene:
         _check(load_library().lsnif_scene_query(self.h, rays.data_ptr(), n, mode, out.data_ptr(),
                                                 _stream_ptr(stream)))
         return out
+
+    def render(self, camera: dict, lights, environment, cfg: dict, world_diag, stream=None,
+               stats: dict | None = None):
+        """render() (renderer.cpp:453-542), PrimaryMode::lsnif: (H, W, 3) float32
+        CUDA tensor, the spp-averaged image. `stats` (a dict) receives the ray
+        counts of the call."""
+        torch = _torch()
+        n = len(world_diag)  # checked against the instance count by the library
+        diag = (C.c_float * max(n, 1))(*[float(v) for v in world_diag])
+        la = (Light * max(len(lights), 1))()
+        for i, L in enumerate(lights):
+            la[i].type = 1 if L["type"] == "sphere" else 0
+            la[i].position[:] = L["position"]
+            la[i].radius = L.get("radius", 0.0)
+            la[i].radiance[:] = L["radiance"]
+        env = (C.c_float * 3)(*[float(v) for v in environment])
+        img = torch.empty((cfg["height"], cfg["width"], 3), dtype=torch.float32,
+                          device=f"cuda:{self._models[0].device}")
+        rs = RenderStats()
+        _check(load_library().lsnif_render(self.h, diag, n, C.byref(_camera(camera)), la, len(lights),
+                                           env, C.byref(_config(cfg)), img.data_ptr(), C.byref(rs),
+                                           _stream_ptr(stream)))
+        if stats is not None:
+            stats.update({k: int(getattr(rs, k)) for k, _ in RenderStats._fields_})
+        return img
 
     def close(self):
         if getattr(self, "h", None):

@@ -165,3 +165,54 @@ def c4_world_to_object() -> np.ndarray:
 
 def c4_bounds() -> np.ndarray:
     return np.array([-8.5, -1.5, -4.5, 8.5, 2.5, 4.5], np.float32)
+
+
+# ------------------------------------------------------- render scene (F3)
+
+RENDER_MODELS = ["teapot_seed0", "sphere_seed1", "box_seed3", "torus_seed2"]
+RENDER_CAMERA = dict(position=(0.0, 2.2, 7.0), look_at=(0.0, 0.5, 0.0), up=(0.0, 1.0, 0.0),
+                     vfov_deg=40.0)
+RENDER_LIGHTS = [dict(type="point", position=(3.0, 4.0, 3.0), radiance=(20.0, 20.0, 20.0)),
+                 dict(type="sphere", position=(-2.5, 3.5, 2.0), radius=0.5,
+                      radiance=(8.0, 8.0, 8.0))]
+RENDER_ENV = (0.05, 0.05, 0.08)
+RENDER_PLACEMENT = [(0.0, 0.0, 0.0), (2.6, 0.6, 0.3), (-2.6, 0.6, 0.2), (0.0, 0.35, -2.4)]
+
+
+def render_world_to_object() -> np.ndarray:
+    """(4, 3, 4) world_to_object of the render scene: translations (pure
+    translation keeps the frame box axis-aligned in the world)."""
+    out = np.zeros((len(RENDER_PLACEMENT), 3, 4), np.float32)
+    for i, p in enumerate(RENDER_PLACEMENT):
+        out[i, :, :3] = np.eye(3)
+        out[i, :, 3] = -np.asarray(p, np.float32)
+    return out
+
+
+def world_diag_from_frames(aabbs) -> list[float]:
+    """PreparedObject::world_diag stand-in: the diagonal of each instance's
+    frame box (the mesh bounds are not part of the model file; translation
+    only, so world and object diagonals agree)."""
+    out = []
+    for a in aabbs:
+        a = np.asarray(a, np.float32)
+        e = a[3:] - a[:3]
+        out.append(float(np.float32(np.sqrt(np.float32((e[0] * e[0] + e[1] * e[1]) + e[2] * e[2])))))
+    return out
+
+
+def glossy_copy(src: str, dst: str, material: int, roughness: float) -> str:
+    """Copies an LSNF v1 file, switching material slot `material` to glossy
+    (MaterialKind 1) with `roughness` — to exercise shade_hit's Phong branch."""
+    import struct
+    b = bytearray(open(src, "rb").read())
+    for n in range(1, 65):  # material block: u32 count, n x {3 f32 albedo, u32 kind, f32 rough}
+        off = len(b) - 24 - 20 * n - 4
+        if off > 0 and struct.unpack_from("<I", b, off)[0] == n:
+            break
+    else:
+        raise ValueError("no material table found")
+    assert 0 <= material < n
+    struct.pack_into("<If", b, off + 4 + 20 * material + 12, 1, roughness)
+    open(dst, "wb").write(bytes(b))
+    return dst
