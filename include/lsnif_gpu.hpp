@@ -8,6 +8,11 @@
 //   lsnif::gpu::intersect        ~ the narrow phase + accept of intersect_scene
 //                                  for one object (renderer.cpp:269-303)
 //   lsnif::gpu::occluded_batch   ~ occluded_batch (renderer.cpp:305-323)
+//   lsnif::gpu::Scene            ~ the LSNIF objects of PreparedScene
+//                                  (renderer.hpp:80-131): intersect_scene /
+//                                  occluded_batch over world rays
+//   lsnif::gpu::render           ~ render() (renderer.cpp:453-542),
+//                                  PrimaryMode::lsnif
 // Errors are rethrown as the reference's exception types:
 // std::invalid_argument for LSNIF_INVALID_ARGUMENT, std::runtime_error
 // otherwise.
@@ -15,6 +20,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -143,6 +149,73 @@ inline std::vector<char> occluded_batch(const Model& model, const std::vector<ls
   const std::vector<lsnif_hit> hits = query(model, rays, LSNIF_QUERY_ANY);
   std::vector<char> out(hits.size(), 0);
   for (size_t i = 0; i < hits.size(); ++i) out[i] = (hits[i].flags_material & LSNIF_HIT_ACCEPTED) ? 1 : 0;
+  return out;
+}
+
+// The LSNIF objects of a PreparedScene: instances (model, world_to_object)
+// in object order. Models are shared, as PreparedScene::prepare caches them.
+class Scene {
+ public:
+  Scene(const std::vector<Model>& models, const std::vector<std::array<float, 12>>& world_to_object)
+      : models_(models) {
+    if (models.size() != world_to_object.size()) throw std::invalid_argument("one transform per instance");
+    std::vector<lsnif_instance> inst(models.size());
+    for (size_t i = 0; i < models.size(); ++i) {
+      inst[i].model = models[i].handle();
+      for (int k = 0; k < 12; ++k) inst[i].world_to_object[k] = world_to_object[i][static_cast<size_t>(k)];
+    }
+    lsnif_scene s = nullptr;
+    check(lsnif_scene_create(inst.data(), static_cast<int32_t>(inst.size()), &s));
+    h_.reset(s, [](lsnif_scene p) { lsnif_scene_destroy(p); });
+  }
+  lsnif_scene handle() const { return h_.get(); }
+  size_t size() const { return models_.size(); }
+
+  // intersect_scene (renderer.cpp:269-303) / occluded_batch (305-323) for a
+  // scene without triangle objects; WORLD-space host rays.
+  std::vector<lsnif_scene_hit> query(const std::vector<lsnif_ray>& rays, int mode) const {
+    const size_t n = rays.size();
+    DeviceBuffer<lsnif_ray> dr(n);
+    DeviceBuffer<lsnif_scene_hit> dh(n);
+    std::vector<lsnif_scene_hit> out(n);
+    if (n) cudaMemcpy(dr.ptr, rays.data(), n * sizeof(lsnif_ray), cudaMemcpyHostToDevice);
+    check(lsnif_scene_query(h_.get(), dr.ptr, static_cast<int64_t>(n), mode, dh.ptr, nullptr));
+    if (n) cudaMemcpy(out.data(), dh.ptr, n * sizeof(lsnif_scene_hit), cudaMemcpyDeviceToHost);
+    return out;
+  }
+  std::vector<std::optional<lsnif_scene_hit>> intersect_scene(const std::vector<lsnif_ray>& rays) const {
+    const auto hits = query(rays, LSNIF_QUERY_CLOSEST);
+    std::vector<std::optional<lsnif_scene_hit>> out(hits.size());
+    for (size_t i = 0; i < hits.size(); ++i)
+      if (hits[i].flags & 1u) out[i] = hits[i];
+    return out;
+  }
+  std::vector<char> occluded_batch(const std::vector<lsnif_ray>& rays) const {
+    const auto hits = query(rays, LSNIF_QUERY_ANY);
+    std::vector<char> out(hits.size());
+    for (size_t i = 0; i < hits.size(); ++i) out[i] = (hits[i].flags & 1u) ? 1 : 0;
+    return out;
+  }
+
+ private:
+  std::vector<Model> models_;
+  std::shared_ptr<lsnif_scene_s> h_;
+};
+
+// render() (renderer.cpp:453-542) with PrimaryMode::lsnif: returns the
+// image as width * height RGB triples (the reference's Image::pixels).
+inline std::vector<float> render(const Scene& scene, const std::vector<float>& world_diag,
+                                 const lsnif_camera& camera, const std::vector<lsnif_light>& lights,
+                                 const float environment[3], const lsnif_render_config& config,
+                                 lsnif_render_stats* stats = nullptr) {
+  const size_t px = static_cast<size_t>(config.width > 0 ? config.width : 0) *
+                    static_cast<size_t>(config.height > 0 ? config.height : 0);
+  DeviceBuffer<float> img(3 * px);
+  check(lsnif_render(scene.handle(), world_diag.data(), static_cast<int32_t>(world_diag.size()), &camera,
+                     lights.data(), static_cast<int32_t>(lights.size()), environment, &config, img.ptr, stats,
+                     nullptr));
+  std::vector<float> out(3 * px);
+  if (px) cudaMemcpy(out.data(), img.ptr, out.size() * sizeof(float), cudaMemcpyDeviceToHost);
   return out;
 }
 
