@@ -86,7 +86,7 @@ struct Workspace {
   size_t x_tiles = 0;
   RowMeta* meta = nullptr;
   size_t meta_cap = 0;
-  int32_t* counter = nullptr;
+  uint8_t* counters = nullptr;  // per chunk: u64 batch counter + one i32 row counter per K bin
   unsigned long long* stats = nullptr;
   int64_t last_rays = 0;
   // profiling: event pairs around each launch (kind 0 trace, 1 mlp)
@@ -141,10 +141,12 @@ int64_t host_chunk() {
   const long long v = e ? std::atoll(e) : 0;
   return v >= 1024 ? static_cast<int64_t>(v) : kHostChunk;
 }
-constexpr size_t kMaxChunks = 4096;                // row counters per query (2^31 rays)
-// counter block, zeroed by one memset per query: 4 x u64 stats | u32 row
-// counter per chunk | u64 batch counter per chunk
-constexpr size_t kCounterBytes = 32 + 4 * kMaxChunks + 8 * kMaxChunks;
+constexpr size_t kMaxChunks = 1024;                // chunks per query (2^31 rays / kChunk)
+// Counter block, zeroed by one memset per query (only the chunks it uses):
+// 4 x u64 stats, then per chunk {u64 batch counter, i32 row counter per K bin}.
+constexpr size_t kStatsBytes = 32;
+constexpr size_t kChunkCounterBytes = 8 + 4 * lsnif_dev::kMaxBins + 8;  // 80 B
+constexpr size_t kCounterBytes = kStatsBytes + kChunkCounterBytes * kMaxChunks;
 
 }  // namespace
 
@@ -182,30 +184,26 @@ struct lsnif_model_s {
     auto& slot = ws[st];
     if (!slot) {
       slot = std::make_unique<Workspace>();
-      // one allocation, reset by a single memset per query: stats (4 x u64)
-      // followed by one row counter per chunk
+      // one allocation, reset by a single memset per query
       ck(cudaMalloc(&slot->stats, kCounterBytes), "cudaMalloc(counters)");
-      slot->counter = reinterpret_cast<int32_t*>(slot->stats + 4);
+      slot->counters = reinterpret_cast<uint8_t*>(slot->stats) + kStatsBytes;
     }
     Workspace& w = *slot;
+    // X / meta: one region per K bin, each able to hold every row of a chunk
     const int64_t rows = std::min<int64_t>(n, kChunk);
     const size_t tiles = static_cast<size_t>((rows + kTileM - 1) / kTileM);
     if (tiles > w.x_tiles) {
       cudaFree(w.X);
-      w.X = nullptr;
-      ck(cudaMalloc(&w.X, tiles * tile_bytes()), "cudaMalloc(X)");
-      w.x_tiles = tiles;
-    }
-    if (static_cast<size_t>(rows) > w.meta_cap) {
       cudaFree(w.meta);
+      w.X = nullptr;
       w.meta = nullptr;
-      ck(cudaMalloc(&w.meta, static_cast<size_t>(rows) * sizeof(RowMeta)), "cudaMalloc(meta)");
-      w.meta_cap = static_cast<size_t>(rows);
+      ck(cudaMalloc(&w.X, lsnif_dev::bin_x_offset(dm.n_bins, static_cast<int64_t>(tiles))), "cudaMalloc(X)");
+      ck(cudaMalloc(&w.meta, static_cast<size_t>(dm.n_bins) * tiles * kTileM * sizeof(RowMeta)),
+         "cudaMalloc(meta)");
+      w.x_tiles = tiles;
     }
     return w;
   }
-
-  uint32_t tile_bytes() const { return static_cast<uint32_t>(kTileM) * dm.K1P * 2; }
 };
 
 namespace {
@@ -231,8 +229,9 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
   const int n_out = 8 + d.n_mat;
   if (n_out > 16) fail(LSNIF_UNSUPPORTED, "n_mat > 8 is not supported");
   const int K1 = H * L * F;
-  const int K1P = (K1 + 1 + 15) / 16 * 16;
-  if (K1P > hid + 16) fail(LSNIF_UNSUPPORTED, "input width H*L*F must be < hidden + 16");
+  const int K1P = (K1 + 15) / 16 * 16;
+  if (K1P > hid + 16) fail(LSNIF_UNSUPPORTED, "input width H*L*F must be <= hidden + 16");
+  if (K1P / 16 > lsnif_dev::kMaxBins) fail(LSNIF_UNSUPPORTED, "input width H*L*F must be <= 256");
 
   DevModel& m = M.dm;
   m = DevModel{};
@@ -250,6 +249,7 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
   m.LF = L * F;
   m.K1 = K1;
   m.K1P = K1P;
+  m.n_bins = K1P / 16;
   m.M = d.table_size;
   m.M_pow2 = (d.table_size & (d.table_size - 1)) == 0;
   m.M_mask = d.table_size - 1;
@@ -338,7 +338,7 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
   M.info.activation_scale = m.act_scale;
 
   // UMMA canonical fp16 operands with the bias folded in as column K:
-  //   W1: hid x K1P (col K1 = b1), W2: hid x (hid+16) (col hid = b2),
+  //   W1: hid x (K1P+16) (col K1P = b1), W2: hid x (hid+16) (col hid = b2),
   //   W3: 16 x hid (rows >= n_out zero).
   const int K2 = hid + 16;
   auto canon = [&](int rows, int cols, auto&& get) {
@@ -350,9 +350,11 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
       }
     return buf;
   };
-  const auto c1 = canon(hid, K1P, [&](int r, int c) -> uint16_t {
+  // W1's bias lives in its own trailing 16-column slab (column K1P = b1),
+  // multiplied by a constant A slab, so an X tile can stop at its K bin
+  const auto c1 = canon(hid, K1P + 16, [&](int r, int c) -> uint16_t {
     if (c < K1) return d.w1[static_cast<size_t>(r) * K1 + c];
-    return c == K1 ? d.b1[r] : uint16_t(0);
+    return c == K1P ? d.b1[r] : uint16_t(0);
   });
   const auto c2 = canon(hid, K2, [&](int r, int c) -> uint16_t {
     if (c < hid) return d.w2[static_cast<size_t>(r) * hid + c];
@@ -564,7 +566,9 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
   ck(cudaSetDevice(M.device), "cudaSetDevice");
   Workspace& w = M.workspace(st, std::max<int64_t>(n, 1));
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
-  ck(cudaMemsetAsync(w.stats, 0, kCounterBytes, st), "cudaMemsetAsync");
+  if (static_cast<size_t>(nchunks) > kMaxChunks) fail(LSNIF_INVALID_ARGUMENT, "too many rays in one call");
+  ck(cudaMemsetAsync(w.stats, 0, kStatsBytes + kChunkCounterBytes * std::max<int64_t>(nchunks, 1), st),
+     "cudaMemsetAsync");
   w.last_rays = n;
   for (int64_t s = 0, ci = 0; s < n; s += kChunk, ++ci) {
     const int64_t cn = std::min(kChunk, n - s);
@@ -578,10 +582,11 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     tp.out = d_hits + s;
     tp.X = w.X;
     tp.meta = w.meta;
-    tp.row_counter = w.counter + ci;
-    tp.batch_counter = reinterpret_cast<unsigned long long*>(w.counter + kMaxChunks) + ci;
+    uint8_t* cc = w.counters + kChunkCounterBytes * ci;
+    tp.batch_counter = reinterpret_cast<unsigned long long*>(cc);
+    tp.row_counter = reinterpret_cast<int32_t*>(cc + 8);
+    tp.cap_tiles = static_cast<int64_t>(w.x_tiles);
     tp.stats = w.stats;
-    tp.tile_bytes = M.tile_bytes();
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (M.profiling) {
       e0 = w.take_event();
@@ -598,16 +603,16 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     mp.m = M.dm;
     mp.X = w.X;
     mp.meta = w.meta;
-    mp.row_counter = w.counter + ci;
+    mp.row_counter = reinterpret_cast<int32_t*>(cc + 8);
+    mp.cap_tiles = static_cast<int64_t>(w.x_tiles);
     mp.out = d_hits + s;
-    mp.tile_bytes = M.tile_bytes();
     mp.mode = mode;
 
     if (M.profiling) {
       e0 = w.take_event();
       ck(cudaEventRecord(e0, st), "cudaEventRecord");
     }
-    ck(lsnif_dev::launch_mlp(mp, static_cast<int>((cn + kTileM - 1) / kTileM), M.num_sms, st),
+    ck(lsnif_dev::launch_mlp(mp, static_cast<int>((cn + kTileM - 1) / kTileM) + M.dm.n_bins, M.num_sms, st),
        "mlp_tc_kernel");
     ++w.launches[1];
     if (M.profiling) {
@@ -822,10 +827,13 @@ lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_
     ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventRecord(ev, static_cast<cudaStream_t>(stream)), "cudaEventRecord");
     for (int i = 0; i < kSlots; ++i) ck(cudaStreamWaitEvent(S.streams[i], ev, 0), "cudaStreamWaitEvent");
+    // At least ~8 chunks per call so the H2D of one chunk, the kernels of the
+    // previous and the D2H of the one before overlap even for small batches.
+    const int64_t step = std::min(S.cap, std::max<int64_t>(16384, ((n + 7) / 8 + 1023) / 1024 * 1024));
     int64_t k = 0;
-    for (int64_t s = 0; s < n; s += S.cap, ++k) {
+    for (int64_t s = 0; s < n; s += step, ++k) {
       const int slot = static_cast<int>(k % kSlots);
-      const int64_t cn = std::min(S.cap, n - s);
+      const int64_t cn = std::min(step, n - s);
       cudaStream_t st = S.streams[slot];
       ck(cudaMemcpyAsync(S.d_rays[slot], h_rays + s, cn * sizeof(lsnif_ray), cudaMemcpyHostToDevice, st),
          "cudaMemcpyAsync(H2D)");
@@ -872,13 +880,13 @@ lsnif_status lsnif_debug_traverse(lsnif_model model, const lsnif_ray* d_rays, in
     ck(cudaMemsetAsync(hidx, 0xff, n * H * L * 8 * 4, st), "memset");
     ck(cudaMemsetAsync(feat, 0, n * static_cast<size_t>(m.K1) * 4, st), "memset");
     Workspace& w = model->workspace(st, 1);
-    ck(cudaMemsetAsync(w.stats, 0, kCounterBytes, st), "cudaMemsetAsync");
+    ck(cudaMemsetAsync(w.stats, 0, kStatsBytes + kChunkCounterBytes, st), "cudaMemsetAsync");
     lsnif_dev::TraceParams tp{};
     tp.m = m;
     tp.rays = d_rays;
     tp.n = n;
-    tp.row_counter = w.counter;
-    tp.batch_counter = reinterpret_cast<unsigned long long*>(w.counter + kMaxChunks);
+    tp.batch_counter = reinterpret_cast<unsigned long long*>(w.counters);
+    tp.row_counter = reinterpret_cast<int32_t*>(w.counters + 8);
     tp.stats = w.stats;
     tp.info = info;
     tp.interval = interval;

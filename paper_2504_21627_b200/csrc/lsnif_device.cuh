@@ -21,6 +21,17 @@ namespace lsnif_dev {
 constexpr int kMaxLevels = 4;
 constexpr int kMaxHitCap = 32;
 constexpr int kTileM = 128;  // rays per MMA tile (TMEM lanes)
+// MLP rows are binned by their used input width: bin b holds the rows whose
+// count * L * F features fit in K_b = 16 (b + 1) columns, so a tile of bin b
+// is stored, loaded and multiplied with K_b columns instead of the padded
+// input width.
+constexpr int kMaxBins = 16;
+constexpr uint32_t kBinTileBytes = kTileM * 16 * 2;  // one 16-column slab of a tile
+
+// Byte offset of bin b's tile region when every bin holds cap_tiles tiles.
+__device__ __host__ __forceinline__ uint64_t bin_x_offset(int b, int64_t cap_tiles) {
+  return static_cast<uint64_t>(b) * (b + 1) / 2 * static_cast<uint64_t>(cap_tiles) * kBinTileBytes;
+}
 
 // Per-model constants, passed by value to every kernel (in the constant
 // parameter bank). Pointers are device memory owned by the model.
@@ -48,6 +59,7 @@ struct DevModel {
   int n_materials;
   float z_zero[32];                    // logits of the all-zero input (rays without points)
   float b3[16];                        // output bias, added in fp32 by the decode epilogue
+  int n_bins;                          // K1P / 16
   // decode_hit of z_zero with enter = 0, exit = 1 (computed on the device at
   // load): rays with a pair but no point differ only in t_world and accept
   float zero_lt;                       // sigmoid(z_zero[1])

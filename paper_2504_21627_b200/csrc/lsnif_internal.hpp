@@ -34,12 +34,12 @@ struct TraceParams {
   int64_t offset;             // first ray of this launch within the query
   int mode;
   lsnif_hit* out;
-  uint8_t* X;                 // compacted MLP operand tiles
-  RowMeta* meta;
-  int32_t* row_counter;
+  uint8_t* X;                 // compacted MLP operand tiles, per K bin (bin_x_offset)
+  RowMeta* meta;              // bin b's rows at meta + b * cap_tiles * 128
+  int32_t* row_counter;       // one per K bin
+  int64_t cap_tiles;          // tiles per bin region
   unsigned long long* batch_counter;  // dynamic 32-ray batch claims (zeroed per launch)
   unsigned long long* stats;  // pairs, rows, points, volume points
-  uint32_t tile_bytes;
   // debug probe (DEBUG=true only)
   int32_t* info;
   float* interval;
@@ -54,9 +54,9 @@ struct MlpParams {
   DevModel m;
   const uint8_t* X;
   const RowMeta* meta;
-  const int32_t* row_counter;
+  const int32_t* row_counter;  // one per K bin
+  int64_t cap_tiles;
   lsnif_hit* out;
-  uint32_t tile_bytes;
   int mode;
 };
 

@@ -134,17 +134,19 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
       P.interval[2 * ray_idx + 1] = pair ? exit : 0.0f;
     }
 
-    // ---- row allocation (warp-aggregated) for rays that need the MLP
+    // ---- row allocation (warp-aggregated per K bin) for rays that need the MLP
     const bool valid = pair && count > 0;
-    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    const int bin = valid ? (count * LF + 15) / 16 - 1 : -1;
     int row = 0;
     if (!DEBUG) {
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      const int leader = __ffs(peers) - 1;
       int base = 0;
-      if (lane == 0 && vmask) base = atomicAdd(P.row_counter, __popc(vmask));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      row = base + __popc(vmask & ((1u << lane) - 1u));
+      if (valid && lane == leader) base = atomicAdd(P.row_counter + bin, __popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      row = base + __popc(peers & ((1u << lane) - 1u));
       if (valid) {
-        float4* dst = reinterpret_cast<float4*>(P.meta + row);
+        float4* dst = reinterpret_cast<float4*>(P.meta + static_cast<int64_t>(bin) * P.cap_tiles * kTileM + row);
         dst[0] = make_float4(__int_as_float(static_cast<int32_t>(ray_idx)), enter, exit, t_min);
         dst[1] = make_float4(t_max, 0.0f, 0.0f, 0.0f);
       }
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
 
     if (valid) {
       lane_ray[2 * lane] = make_float4(w.o[0], w.o[1], w.o[2], __int_as_float(row));
-      lane_ray[2 * lane + 1] = make_float4(w.d[0], w.d[1], w.d[2], 0.0f);
+      lane_ray[2 * lane + 1] = make_float4(w.d[0], w.d[1], w.d[2], __int_as_float(bin));
     }
     __syncwarp();
     // ---- warp-cooperative encode of all pooled points (encoding.hpp:166-176)
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
       const float4 rq = lane_ray[2 * owner], rr = lane_ray[2 * owner + 1];
       const float ro[3] = {rq.x, rq.y, rq.z}, rd[3] = {rr.x, rr.y, rr.z};
       const int o_row = __float_as_int(rq.w);
+      const int o_bin = __float_as_int(rr.w);
       const int k = j - o_excl;
       const uint2 e = pool[k * 32 + owner];
       float p[3];
@@ -249,7 +252,8 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
         P.pts[(o_ray * H + k) * 3 + 1] = p[1];
         P.pts[(o_ray * H + k) * 3 + 2] = p[2];
       } else {
-        uint8_t* tile = P.X + static_cast<int64_t>(o_row >> 7) * P.tile_bytes;
+        uint8_t* tile = P.X + bin_x_offset(o_bin, P.cap_tiles) +
+                        static_cast<int64_t>(o_row >> 7) * (o_bin + 1) * kBinTileBytes;
         const int r = o_row & 127;
         const int col0 = k * LF;
         if ((LF & 1) == 0) {
@@ -267,24 +271,16 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
       }
     }
 
-    // ---- zero padding of the row tail + bias constant column (encoding.hpp:170)
+    // ---- zero padding of the row tail up to the bin width (encoding.hpp:170)
     if (!DEBUG && valid) {
-      uint8_t* tile = P.X + static_cast<int64_t>(row >> 7) * P.tile_bytes;
+      uint8_t* tile = P.X + bin_x_offset(bin, P.cap_tiles) + static_cast<int64_t>(row >> 7) * (bin + 1) * kBinTileBytes;
       const int r = row & 127;
-      const __half hs = __float2half_rn(scale);
-      const __half hz = __float2half_rn(0.0f);
+      const int kb = 16 * (bin + 1);
       int col = count * LF;
-      for (; col < m.K1P && (col & 7); ++col)
-        *reinterpret_cast<__half*>(tile + canon_offset(r, col, kTileM)) = (col == m.K1) ? hs : hz;
-      for (; col < m.K1P; col += 8) {
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        const int q = m.K1 - col;
-        if (q >= 0 && q < 8) {
-          const uint32_t hbits = static_cast<uint32_t>(__half_as_ushort(hs)) << ((q & 1) * 16);
-          if (q < 2) v.x = hbits; else if (q < 4) v.y = hbits; else if (q < 6) v.z = hbits; else v.w = hbits;
-        }
-        *reinterpret_cast<uint4*>(tile + canon_offset(r, col, kTileM)) = v;
-      }
+      if ((col & 1) == 0)
+        for (; col < kb && (col & 7); col += 2) *reinterpret_cast<uint32_t*>(tile + canon_offset(r, col, kTileM)) = 0u;
+      for (; col < kb && (col & 7); ++col) *reinterpret_cast<uint16_t*>(tile + canon_offset(r, col, kTileM)) = 0;
+      for (; col < kb; col += 8) *reinterpret_cast<uint4*>(tile + canon_offset(r, col, kTileM)) = make_uint4(0u, 0u, 0u, 0u);
     }
     __syncwarp();  // pool reuse by the next batch
   }
@@ -336,8 +332,9 @@ __device__ __forceinline__ uint32_t leaky_pack(uint32_t a, uint32_t b) {
 }
 
 // h = leaky(D) for hidden columns [c0, c0 + 64) of this lane's row -> packed
-// fp16 pairs in A_h columns [c0/2, c0/2 + 32). The bias is already in D and
-// the activation scale carries through the positively homogeneous leaky-ReLU.
+// fp16 pairs in A_h columns [c0/2, c0/2 + 32). The bias is already in D (a
+// constant-operand K-step) and the activation scale carries through the
+// positively homogeneous leaky-ReLU.
 __device__ __forceinline__ void epi_hidden64(uint32_t tD, uint32_t tA, int c0) {
   uint32_t a0[32], a1[32], o[32];
   tc::tmem_ld32(tD + c0, a0);
@@ -377,7 +374,8 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   uint8_t* sW1 = base;
   uint8_t* sW2 = sW1 + m.w1_bytes;
   uint8_t* sW3 = sW2 + m.w2_bytes;
-  uint8_t* sX = sW3 + ((m.w3_bytes + 1023) & ~1023u);
+  uint8_t* sC = sW3 + ((m.w3_bytes + 1023) & ~1023u);  // constant bias slab (4 KB)
+  uint8_t* sX = sC + kBinTileBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sX + NS * xstage);
   uint64_t* w_full = bars;                // 1
   uint64_t* x_full = bars + 1;            // NS
@@ -386,10 +384,36 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   uint64_t* h_ready = l_done + 2;         // 2
   uint64_t* acc_free = h_ready + 2;       // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
+  int* tstart = reinterpret_cast<int*>(tmem_slot + 4);  // first global tile of each K bin (+ total)
+  int* x_bin = tstart + kMaxBins + 1;  // K bin of the tile in each X stage (loader -> MMA)
 
-  const int rows = *P.row_counter;
-  const int ntiles = (rows + kTileM - 1) / kTileM;
+  // tiles of all K bins, bin-major: global tile -> (bin b, tile t within b)
+  const int nb = m.n_bins;
+  int ntiles = 0;
+  for (int b = 0; b < nb; ++b) ntiles += (P.row_counter[b] + kTileM - 1) / kTileM;
   if (static_cast<int>(blockIdx.x) >= ntiles) return;
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      tstart[b] = acc;
+      acc += (P.row_counter[b] + kTileM - 1) / kTileM;
+    }
+    tstart[nb] = acc;
+  }
+  // constant A slab of layer 1's bias K-step: column 0 = act_scale, 128 rows
+  // (W1's last 16-column slab holds b1 in column 0)
+  for (int r = threadIdx.x; r < kTileM; r += blockDim.x) {
+    const uint32_t hs = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(m.act_scale)));
+    *reinterpret_cast<uint4*>(sC + canon_offset(r, 0, kTileM)) = make_uint4(hs, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(sC + canon_offset(r, 8, kTileM)) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  tc::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
+  auto locate = [&](int tile, int& b, int& t) {
+    b = 0;
+    while (tile >= tstart[b + 1]) ++b;
+    t = tile - tstart[b];
+  };
+  const int64_t bin_rows = P.cap_tiles * kTileM;
   const int my_tiles = (ntiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
                        static_cast<int>(gridDim.x);
 
@@ -423,16 +447,28 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       tc::bulk_g2s(sW2, m.w_canon + m.w1_bytes, m.w2_bytes, w_full);
       tc::bulk_g2s(sW3, m.w_canon + m.w1_bytes + m.w2_bytes, m.w3_bytes, w_full);
       constexpr int kPrefetch = 8;
-      for (int i = 0; i < kPrefetch && i < my_tiles; ++i)
-        tc::bulk_prefetch_l2(P.X + static_cast<int64_t>(blockIdx.x + i * gridDim.x) * P.tile_bytes, xbytes);
+      auto tile_src = [&](int i, uint32_t& bytes) -> const uint8_t* {
+        int b, t;
+        locate(blockIdx.x + i * gridDim.x, b, t);
+        bytes = (b + 1) * kBinTileBytes;
+        return P.X + bin_x_offset(b, P.cap_tiles) + static_cast<int64_t>(t) * bytes;
+      };
+      uint32_t nbytes;
+      for (int i = 0; i < kPrefetch && i < my_tiles; ++i) {
+        const uint8_t* src = tile_src(i, nbytes);
+        tc::bulk_prefetch_l2(src, nbytes);
+      }
       for (int i = 0; i < my_tiles; ++i) {
-        const int tile = blockIdx.x + i * gridDim.x;
         const int st = i % NS, k = i / NS;
-        if (i + kPrefetch < my_tiles)
-          tc::bulk_prefetch_l2(P.X + static_cast<int64_t>(tile + kPrefetch * gridDim.x) * P.tile_bytes, xbytes);
+        if (i + kPrefetch < my_tiles) {
+          const uint8_t* src = tile_src(i + kPrefetch, nbytes);
+          tc::bulk_prefetch_l2(src, nbytes);
+        }
+        const uint8_t* src = tile_src(i, nbytes);
         if (k > 0) tc::mbar_wait(x_empty + st, (k - 1) & 1);
-        tc::mbar_arrive_expect_tx(x_full + st, xbytes);
-        tc::bulk_g2s(sX + st * xstage, P.X + static_cast<int64_t>(tile) * P.tile_bytes, xbytes, x_full + st);
+        x_bin[st] = static_cast<int>(nbytes / kBinTileBytes) - 1;  // released by the arrive below
+        tc::mbar_arrive_expect_tx(x_full + st, nbytes);
+        tc::bulk_g2s(sX + st * xstage, src, nbytes, x_full + st);
       }
     }
   } else if (warp == 1) {
@@ -440,7 +476,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     if (lane == 0) {
       tc::mbar_wait(w_full, 0);
       const uint32_t sW1_a = tc::smem_addr(sW1), sW2_a = tc::smem_addr(sW2), sW3_a = tc::smem_addr(sW3);
-      const uint32_t sX_a = tc::smem_addr(sX);
+      const uint32_t sX_a = tc::smem_addr(sX), sC_a = tc::smem_addr(sC);
       constexpr uint32_t kIdescH = tc::idesc_f16_f32(kTileM, HID);
       const uint32_t idesc3 = tc::idesc_f16_f32(kTileM, m.N3);
       constexpr uint32_t a_lbo = kTileM * 16;
@@ -459,10 +495,17 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
             if (ka > 0 && !mbar_test(acc_free + g, (ka - 1) & 1)) continue;
             tc::tc_fence_after();
             const uint32_t a_base = sX_a + st * xstage;
-            for (int ks = 0; ks < m.K1P / 16; ++ks) {  // L1: A = X (SMEM)
+            const int xb = x_bin[st];
+            for (int ks = 0; ks <= xb; ++ks) {  // L1: A = X (SMEM), the tile's bin width
+              // (the tile's SMEM stage holds K_b columns: LBO stays 128 x 16 B)
               const uint64_t ad = tc::smem_desc(a_base + ks * 2 * a_lbo, a_lbo, 128);
               const uint64_t bd = tc::smem_desc(sW1_a + ks * 2 * HID * 16, HID * 16, 128);
               tc::mma_f16_ss(tD, ad, bd, kIdescH, ks > 0 ? 1u : 0u);
+            }
+            {  // + b1: constant slab (act_scale in column 0) x W1's bias slab
+              const uint64_t ad = tc::smem_desc(sC_a, a_lbo, 128);
+              const uint64_t bd = tc::smem_desc(sW1_a + (m.K1P / 16) * 2 * HID * 16, HID * 16, 128);
+              tc::mma_f16_ss(tD, ad, bd, kIdescH, 1u);
             }
             tc::mma_commit(x_empty + st);
             gl[g] = 1;
@@ -506,11 +549,13 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     }
     uint32_t lcount = 0;
     for (int i = g; i < my_tiles; i += 2) {
-      const int tile = blockIdx.x + i * gridDim.x;
-      const int grow = tile * kTileM + row;
+      int tb, tt;
+      locate(blockIdx.x + i * gridDim.x, tb, tt);
+      const int grow = tt * kTileM + row;
+      const bool live = grow < P.row_counter[tb];
       float4 ma = make_float4(0, 0, 0, 0), mb = ma;  // row metadata, prefetched
-      if (half == 0 && grow < rows) {
-        const float4* mp = reinterpret_cast<const float4*>(P.meta + grow);
+      if (half == 0 && live) {
+        const float4* mp = reinterpret_cast<const float4*>(P.meta + tb * bin_rows + grow);
         ma = __ldg(mp);
         mb = __ldg(mp + 1);
       }
@@ -538,7 +583,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(acc_free + g);
-      if (half == 0 && grow < rows) {
+      if (half == 0 && live) {
         lsnif_hit hh;
         decode_hit(z, m.n_mat, m.occ_threshold, ma.y, ma.z, ma.w, mb.x, P.mode, true, hh);
         store_hit(P.out + __float_as_int(ma.x), hh);
@@ -761,7 +806,9 @@ size_t trace_smem_bytes(const DevModel& m) {
 
 size_t mlp_smem_bytes(const DevModel& m) {
   const size_t x = (static_cast<size_t>(kTileM) * m.K1P * 2 + 1023) & ~size_t(1023);
-  return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + MlpLayout<128>::kXStages * x + 256;
+  // + barriers, TMEM slot, bin tile starts and the scaled b1 (1 KB tail)
+  return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + kBinTileBytes +
+         MlpLayout<128>::kXStages * x + 1024;
 }
 
 // Per-(kernel, device, smem size) launch configuration, computed once: the
