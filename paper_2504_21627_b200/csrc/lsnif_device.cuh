@@ -432,44 +432,48 @@ __device__ __forceinline__ void encode_volume_level(const DevModel& m, int level
 // apply_heads (mlp.hpp:80-94) + NeuralHit decode (renderer.cpp:211-223) +
 // accept rule (renderer.cpp:281-284 closest / 317-320 any).
 __device__ __forceinline__ float sigmoid_ref(float v) {
-  return __fdiv_rn(1.0f, __fadd_rn(1.0f, expf(-v)));
+  return __frcp_rn(__fadd_rn(1.0f, expf(-v)));  // == 1 / (1 + e^-v), correctly rounded
 }
 
 // The occlusion decision sigmoid(z0) > 0.5 (renderer.cpp:212) is monotone in
 // z0; it is taken as z0 >= occ_threshold, the boundary computed on the host
 // with the reference's (correctly rounded) expf, so it does not depend on the
 // last-ulp behaviour of the device expf.
-__device__ __forceinline__ void decode_hit(const float* z, int n_mat, float occ_threshold,
-                                           float enter, float exit, float t_min, float t_max,
-                                           int mode, bool pair_flag, lsnif_hit& h) {
-  const float lt = sigmoid_ref(z[1]);
-  const bool occluded = z[0] >= occ_threshold;
+// The MLP epilogue splits the decode over the two warps that own a row:
+// decode_flags (visibility, t_world, material, accept flags: z0, z1, z8..)
+// and decode_normal + decode_albedo (z2..z7); decode_hit is all of them.
+// zm points at the n_mat material logits.
+__device__ __forceinline__ void decode_flags(float z0, float z1, const float* zm, int n_mat, float occ_threshold,
+                                             float enter, float exit, float t_min, float t_max, int mode,
+                                             bool pair_flag, uint32_t& flags_material, float& t_world) {
+  const float lt = sigmoid_ref(z1);
+  const bool occluded = z0 >= occ_threshold;
   const float tw = __fadd_rn(enter, __fmul_rn(lt, __fsub_rn(exit, enter)));
-  const float n0 = z[2], n1 = z[3], n2 = z[4];
-  const float len = sqrtf(__fadd_rn(__fadd_rn(__fmul_rn(n0, n0), __fmul_rn(n1, n1)), __fmul_rn(n2, n2)));
-  if (len > 1e-12f) {
-    h.normal[0] = __fdiv_rn(n0, len);
-    h.normal[1] = __fdiv_rn(n1, len);
-    h.normal[2] = __fdiv_rn(n2, len);
-  } else {
-    h.normal[0] = h.normal[1] = h.normal[2] = 0.0f;
-  }
-  h.albedo[0] = sigmoid_ref(z[5]);
-  h.albedo[1] = sigmoid_ref(z[6]);
-  h.albedo[2] = sigmoid_ref(z[7]);
-  float zmax = z[8];
-  for (int k = 1; k < n_mat; ++k) zmax = (z[8 + k] > zmax) ? z[8 + k] : zmax;
+  // (loops unrolled to the compile-time maximum so the logits stay in registers)
+  constexpr int kMaxMat = 8;
+  float zmax = zm[0];
+#pragma unroll
+  for (int k = 1; k < kMaxMat; ++k)
+    if (k < n_mat) zmax = (zm[k] > zmax) ? zm[k] : zmax;
+  float e[kMaxMat];
   float sum = 0.0f;
-  for (int k = 0; k < n_mat; ++k) sum = __fadd_rn(sum, expf(__fsub_rn(z[8 + k], zmax)));
-  int arg = 0;
-  float best = __fdiv_rn(expf(__fsub_rn(z[8], zmax)), sum);
-  for (int k = 1; k < n_mat; ++k) {
-    const float pk = __fdiv_rn(expf(__fsub_rn(z[8 + k], zmax)), sum);
-    if (pk > best) {
-      best = pk;
-      arg = k;
+#pragma unroll
+  for (int k = 0; k < kMaxMat; ++k)
+    if (k < n_mat) {
+      e[k] = expf(__fsub_rn(zm[k], zmax));
+      sum = __fadd_rn(sum, e[k]);
     }
-  }
+  int arg = 0;
+  float best = __fdiv_rn(e[0], sum);
+#pragma unroll
+  for (int k = 1; k < kMaxMat; ++k)
+    if (k < n_mat) {
+      const float pk = __fdiv_rn(e[k], sum);
+      if (pk > best) {
+        best = pk;
+        arg = k;
+      }
+    }
   uint32_t flags = pair_flag ? LSNIF_HIT_PAIR : 0u;
   if (occluded) {
     flags |= LSNIF_HIT_OCCLUDED;
@@ -477,8 +481,34 @@ __device__ __forceinline__ void decode_hit(const float* z, int n_mat, float occ_
                                                       : (tw >= t_min && tw <= t_max);
     if (accept && pair_flag) flags |= LSNIF_HIT_ACCEPTED;
   }
-  h.flags_material = flags | (static_cast<uint32_t>(arg) << LSNIF_HIT_MATERIAL_SHIFT);
-  h.t_world = tw;
+  flags_material = flags | (static_cast<uint32_t>(arg) << LSNIF_HIT_MATERIAL_SHIFT);
+  t_world = tw;
+}
+
+__device__ __forceinline__ void decode_normal(float n0, float n1, float n2, float normal[3]) {
+  const float len = sqrtf(__fadd_rn(__fadd_rn(__fmul_rn(n0, n0), __fmul_rn(n1, n1)), __fmul_rn(n2, n2)));
+  if (len > 1e-12f) {
+    normal[0] = __fdiv_rn(n0, len);
+    normal[1] = __fdiv_rn(n1, len);
+    normal[2] = __fdiv_rn(n2, len);
+  } else {
+    normal[0] = normal[1] = normal[2] = 0.0f;
+  }
+}
+
+__device__ __forceinline__ void decode_albedo(float z5, float z6, float z7, float albedo[3]) {
+  albedo[0] = sigmoid_ref(z5);
+  albedo[1] = sigmoid_ref(z6);
+  albedo[2] = sigmoid_ref(z7);
+}
+
+__device__ __forceinline__ void decode_hit(const float* z, int n_mat, float occ_threshold,
+                                           float enter, float exit, float t_min, float t_max,
+                                           int mode, bool pair_flag, lsnif_hit& h) {
+  decode_flags(z[0], z[1], z + 8, n_mat, occ_threshold, enter, exit, t_min, t_max, mode, pair_flag,
+               h.flags_material, h.t_world);
+  decode_normal(z[2], z[3], z[4], h.normal);
+  decode_albedo(z[5], z[6], z[7], h.albedo);
 }
 
 // decode_hit(m.z_zero, ...) for a pair without boundary points (the all-zero

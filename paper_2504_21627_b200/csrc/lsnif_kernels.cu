@@ -359,6 +359,18 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   return done != 0;
 }
 
+// LSNIF_MLP_TIMELINE builds record, for CTA 0, clock64 stamps of the MMA
+// issuer and of one warp per epilogue half and group (probe builds only).
+#ifdef LSNIF_MLP_TIMELINE
+__device__ unsigned long long g_mlp_timeline[1 << 16];
+#define TL_STAMP(slot) g_mlp_timeline[(slot)] = clock64()
+extern "C" int lsnif_probe_mlp_timeline(unsigned long long* host, int n) {
+  return static_cast<int>(cudaMemcpyFromSymbol(host, g_mlp_timeline, sizeof(unsigned long long) * n));
+}
+#else
+#define TL_STAMP(slot) (void)0
+#endif
+
 template <int HID>
 __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(const MlpParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -386,6 +398,9 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_free + 2);
   int* tstart = reinterpret_cast<int*>(tmem_slot + 4);  // first global tile of each K bin (+ total)
   int* x_bin = tstart + kMaxBins + 1;  // K bin of the tile in each X stage (loader -> MMA)
+  int* bin_rows_n = x_bin + 8;         // rows of each K bin
+  constexpr int kZSlots = 10;          // logits a thread keeps for its deferred decode
+  float* zslots = reinterpret_cast<float*>(sX + NS * xstage + 1024);  // 16 warps x 10 x 32
 
   // tiles of all K bins, bin-major: global tile -> (bin b, tile t within b)
   const int nb = m.n_bins;
@@ -399,6 +414,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       acc += (P.row_counter[b] + kTileM - 1) / kTileM;
     }
     tstart[nb] = acc;
+    for (int b = 0; b < nb; ++b) bin_rows_n[b] = P.row_counter[b];
   }
   // constant A slab of layer 1's bias K-step: column 0 = act_scale, 128 rows
   // (W1's last 16-column slab holds b1 in column 0)
@@ -493,6 +509,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
             const int st = i % NS, kx = i / NS, ka = i >> 1;
             if (!mbar_test(x_full + st, kx & 1)) continue;
             if (ka > 0 && !mbar_test(acc_free + g, (ka - 1) & 1)) continue;
+            if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 5);  // X + accumulator ready seen
             tc::tc_fence_after();
             const uint32_t a_base = sX_a + st * xstage;
             const int xb = x_bin[st];
@@ -508,9 +525,11 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
               tc::mma_f16_ss(tD, ad, bd, kIdescH, 1u);
             }
             tc::mma_commit(x_empty + st);
+            if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 0);
             gl[g] = 1;
           } else {
             if (!mbar_test(h_ready + g, hc[g] & 1)) continue;
+            if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 3 + (gl[g] - 1));  // h1 / h2 ready seen
             ++hc[g];
             tc::tc_fence_after();
             if (gl[g] == 1) {  // L2: A = h1 (TMEM), K = HID + bias block
@@ -519,12 +538,14 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
                 tc::mma_f16_ts(tD, tA + ks * 8, bd, kIdescH, ks > 0 ? 1u : 0u);
               }
               gl[g] = 2;
+              if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 1);
             } else {           // L3: A = h2 (TMEM), K = HID, N = 16
               for (int ks = 0; ks < HID / 16; ++ks) {
                 const uint64_t bd = tc::smem_desc(sW3_a + ks * 2 * m.N3 * 16, m.N3 * 16, 128);
                 tc::mma_f16_ts(tD, tA + ks * 8, bd, idesc3, ks > 0 ? 1u : 0u);
               }
               gl[g] = 0;
+              if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 2);
               gi[g] += 2;
             }
           }
@@ -548,47 +569,102 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
       tc::tmem_wait_st();
     }
     uint32_t lcount = 0;
-    for (int i = g; i < my_tiles; i += 2) {
+    // Row metadata, prefetched one tile ahead: ray index (both halves),
+    // interval and t range (the lower half, which decodes them).
+    auto load_meta = [&](int i, float4& a, float4& b, bool& live) {
+      a = b = make_float4(0.f, 0.f, 0.f, 0.f);
+      live = false;
+      if (i >= my_tiles) return;
       int tb, tt;
       locate(blockIdx.x + i * gridDim.x, tb, tt);
       const int grow = tt * kTileM + row;
-      const bool live = grow < P.row_counter[tb];
-      float4 ma = make_float4(0, 0, 0, 0), mb = ma;  // row metadata, prefetched
-      if (half == 0 && live) {
+      live = grow < bin_rows_n[tb];
+      if (live) {
         const float4* mp = reinterpret_cast<const float4*>(P.meta + tb * bin_rows + grow);
-        ma = __ldg(mp);
-        mb = __ldg(mp + 1);
+        a = __ldg(mp);
+        if (half == 0) b = __ldg(mp + 1);
       }
+    };
+    // The decode of a tile (heads, NeuralHit, accept; renderer.cpp:208-223,
+    // 280-301) is deferred until after the group's next layer-1 epilogue, so
+    // it overlaps the next tile's layer-2 MMAs instead of delaying its
+    // layer 1. The logits wait in this thread's private SMEM slots; the two
+    // warps of a row split the work: lower half z0, z1, z8.. (visibility,
+    // t_world, material, accept), upper half z2..z7 (normal, albedo).
+    float* zs = zslots + (warp - 2) * kZSlots * 32 + lane;
+    float4 pa, pb;  // pending tile's metadata
+    bool plive = false;
+    auto decode_pending = [&]() {
+      if (!plive) return;
+      float* dst = reinterpret_cast<float*>(P.out + __float_as_int(pa.x));
+      if (half == 0) {
+        float zm[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) zm[k] = k < m.n_mat ? zs[(2 + k) * 32] : 0.0f;
+        uint32_t fm;
+        float tw;
+        decode_flags(zs[0], zs[32], zm, m.n_mat, m.occ_threshold, pa.y, pa.z, pa.w, pb.x, P.mode, true, fm, tw);
+        *reinterpret_cast<float2*>(dst) = make_float2(__uint_as_float(fm), tw);
+      } else {
+        float nrm[3], alb[3];
+        decode_normal(zs[0], zs[32], zs[64], nrm);
+        decode_albedo(zs[96], zs[128], zs[160], alb);
+        *reinterpret_cast<float2*>(dst + 2) = make_float2(nrm[0], nrm[1]);
+        *reinterpret_cast<float4*>(dst + 4) = make_float4(nrm[2], alb[0], alb[1], alb[2]);
+      }
+      plive = false;
+    };
+    float4 na, nb_;
+    bool nlive;
+    load_meta(g, na, nb_, nlive);
+    for (int i = g; i < my_tiles; i += 2) {
+      const float4 ma = na, mb = nb_;
+      const bool live = nlive;
+      load_meta(i + 2, na, nb_, nlive);
+      const bool tl = blockIdx.x == 0 && i < 1024 && lane == 0;
+      (void)tl;
 #pragma unroll 1
       for (int layer = 0; layer < 2; ++layer) {  // h1, h2 -> A_h
         tc::mbar_wait(l_done + g, lcount++ & 1);
+        if (tl) TL_STAMP(i * 64 + 8 + 8 * layer + e);  // L1 / L2 done seen by warp e
         tc::tc_fence_after();
         epi_hidden64(tD, tA, half * 64);
         tc::tmem_wait_st();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(h_ready + g);
+        if (tl) TL_STAMP(i * 64 + 24 + 8 * layer + e);  // h1 / h2 published by warp e
+        if (layer == 0) decode_pending();             // previous tile of this group
       }
-      // layer 3 -> heads, decode, accept (renderer.cpp:208-223, 280-301)
+      // layer 3: logits (+ b3 in fp32, activation scale removed) -> SMEM
       tc::mbar_wait(l_done + g, lcount++ & 1);
+      if (tl) TL_STAMP(i * 64 + 40 + e);  // L3 done seen
       tc::tc_fence_after();
-      float z[16];
-      if (half == 0) {
+      {
         uint32_t acc[16];
         tc::tmem_ld16(tD, acc);
         tc::tmem_wait_ld();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(acc_free + g);
+        if (half == 0) {
+          zs[0] = __fadd_rn(__fmul_rn(__uint_as_float(acc[0]), m.inv_act_scale), m.b3[0]);
+          zs[32] = __fadd_rn(__fmul_rn(__uint_as_float(acc[1]), m.inv_act_scale), m.b3[1]);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) z[q] = __fadd_rn(__fmul_rn(__uint_as_float(acc[q]), m.inv_act_scale), m.b3[q]);
+          for (int k = 0; k < 8; ++k)
+            if (k < m.n_mat) zs[(2 + k) * 32] = __fadd_rn(__fmul_rn(__uint_as_float(acc[8 + k]), m.inv_act_scale), m.b3[8 + k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 6; ++k)
+            zs[k * 32] = __fadd_rn(__fmul_rn(__uint_as_float(acc[2 + k]), m.inv_act_scale), m.b3[2 + k]);
+        }
       }
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(acc_free + g);
-      if (half == 0 && live) {
-        lsnif_hit hh;
-        decode_hit(z, m.n_mat, m.occ_threshold, ma.y, ma.z, ma.w, mb.x, P.mode, true, hh);
-        store_hit(P.out + __float_as_int(ma.x), hh);
-      }
+      pa = ma;
+      pb = mb;
+      plive = live;
+      if (tl) TL_STAMP(i * 64 + 48 + e);  // tile's epilogue work done (decode deferred)
     }
+    decode_pending();
   }
   __syncthreads();
   if (warp == 1) {
@@ -808,7 +884,7 @@ size_t mlp_smem_bytes(const DevModel& m) {
   const size_t x = (static_cast<size_t>(kTileM) * m.K1P * 2 + 1023) & ~size_t(1023);
   // + barriers, TMEM slot, bin tile starts and the scaled b1 (1 KB tail)
   return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + kBinTileBytes +
-         MlpLayout<128>::kXStages * x + 1024;
+         MlpLayout<128>::kXStages * x + 1024 + 2 * MlpLayout<128>::kEpiWarps * 10 * 32 * 4;
 }
 
 // Per-(kernel, device, smem size) launch configuration, computed once: the
