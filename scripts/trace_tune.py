@@ -19,25 +19,31 @@ flush = torch.empty(64 << 20, dtype=torch.int32, device="cuda")
 res = []
 for lib in libs:
     gm = lsnif.GpuModel(path, 0)
-    sets = {"c2": lsnif.rays_to_tensor(W.camera_rays(1920, 1080), "cuda"),
+    prim = W.camera_rays(1920, 1080)
+    hits = lsnif.hits_to_numpy(gm.query(lsnif.rays_to_tensor(prim, "cuda")))
+    sets = {"c2": lsnif.rays_to_tensor(prim, "cuda"),
+            "c2shadow": lsnif.rays_to_tensor(W.shadow_rays(prim, hits, gm.aabb)[0], "cuda"),
             "c3": lsnif.rays_to_tensor(W.incoherent_rays(1 << 22, gm.aabb, seed=3), "cuda")}
     for dr in drains:
         os.environ["LSNIF_TRACE_DRAIN"] = dr
         for name, d in sets.items():
-            out = gm.query(d)
+            mode = lsnif.ANY if name == "c2shadow" else lsnif.CLOSEST
+            out = gm.query(d, mode)
+            st = gm.last_stats()
             gm.profile_enable(True)
             for _ in range(3):
-                gm.query(d, out=out)
+                gm.query(d, mode, out=out)
             gm.profile_read(reset=True)
             reps = 10
             for _ in range(reps):
                 flush.add_(1)
-                gm.query(d, out=out)
+                gm.query(d, mode, out=out)
             p = gm.profile_read(reset=True)
             gm.profile_enable(False)
             r = dict(lib=os.path.basename(lib), drain=int(dr), set=name, rays=d.shape[0],
                      trace_ms=p["trace_ms"] / reps, mlp_ms=p["mlp_ms"] / reps)
             r["grays_s_trace"] = d.shape[0] / r["trace_ms"] / 1e6
+            r["stats"] = st
             res.append(r)
             print(json.dumps(r), flush=True)
     gm.close()
