@@ -267,6 +267,75 @@ lsnif_status lsnif_render_debug_paths(const lsnif_camera* camera, const lsnif_re
                                       int64_t first_path, int64_t n, lsnif_ray* d_rays,
                                       float* d_uniforms, int32_t k, void* stream);
 
+/* ---- GPU training ----
+ * lsnif::train (training.cpp:95-230): fresh balanced batches of external and
+ * surface rays labelled against the mesh (the reference's BVH oracle:
+ * closest Moller-Trumbore hit, ties to the lower face), DDA + hash-grid
+ * encode with the current fp32 tables, fp32 forward, composite_loss
+ * (loss.hpp), backward (mlp.hpp:188-225), hash-gradient scatter
+ * (encoding.hpp:193-209) and dense bias-corrected Adam on the MLP and the
+ * tables (mlp.hpp:243-272). Random numbers: per-sample counter streams
+ * (the reference's per-worker sequential mt19937 stream with rejection
+ * retries is inherently serial); same distributions. */
+typedef struct lsnif_mesh_desc {
+  const float* vertices;      /* 3 per vertex (object space) */
+  int32_t n_vertices;
+  const float* normals;       /* 3 per vertex normal; NULL / 0 = geometric normals */
+  int32_t n_normals;
+  const int32_t* faces;       /* 3 vertex indices per triangle */
+  const int32_t* face_normals; /* 3 normal indices per triangle, or NULL */
+  const int32_t* face_material; /* per triangle, index into the model's material table */
+  int32_t n_faces;
+} lsnif_mesh_desc;
+
+typedef struct lsnif_train_config {
+  int32_t batch;        /* TrainConfig::batch */
+  float lr;             /* Adam step size (AdamConfig::lr) */
+  float external_mix;   /* fraction of rays originating outside */
+  uint64_t seed;
+} lsnif_train_config;
+
+typedef struct lsnif_train_loss { /* LossTerms (loss.hpp:25-31), batch means */
+  float total, occlusion_bce, local_t_mae, normal_cosine, albedo_rel_l2, material_ce;
+  int64_t step;
+} lsnif_train_loss;
+
+/* TrainSample targets (training.hpp:15-22) for the batch-gradient probe. */
+typedef struct lsnif_train_target {
+  int32_t occluded;
+  float local_t;
+  float normal[3];
+  float albedo[3];
+  int32_t material;
+} lsnif_train_target;
+
+typedef struct lsnif_trainer_s* lsnif_trainer;
+
+/* `init`: the starting model (e.g. make_sparse_hash_grid + make_mlp, or a
+ * file's contents); its occupancy grid, frame box and materials are kept. */
+lsnif_status lsnif_trainer_create(const lsnif_model_desc* init, const lsnif_mesh_desc* mesh,
+                                  const lsnif_train_config* config, int device, lsnif_trainer* out);
+/* Same, starting from an LSNF v1 file (e.g. the reference's init state saved
+ * with save_model, or a model to fine-tune). */
+lsnif_status lsnif_trainer_create_from_file(const char* path, const lsnif_mesh_desc* mesh,
+                                            const lsnif_train_config* config, int device, lsnif_trainer* out);
+lsnif_status lsnif_trainer_destroy(lsnif_trainer trainer);
+/* Runs `steps` optimizer steps; `last` (nullable) gets the last step's loss. */
+lsnif_status lsnif_trainer_step(lsnif_trainer trainer, int32_t steps, lsnif_train_loss* last, void* stream);
+/* The current parameters as a query model, quantised to binary16 exactly as
+ * save_model + load_model would (model_io.cpp:71-175). */
+lsnif_status lsnif_trainer_export(lsnif_trainer trainer, lsnif_model* out);
+/* Parity probe: loss terms and gradients of a GIVEN batch (object-space rays
+ * + targets, DEVICE), no update. d_grad_mlp: w1|b1|w2|b2|w3|b3 row-major
+ * fp32; d_grad_tables: n_levels x M x F fp32. Either may be NULL. */
+lsnif_status lsnif_trainer_batch_grad(lsnif_trainer trainer, const lsnif_ray* d_rays,
+                                      const lsnif_train_target* d_targets, int64_t n,
+                                      lsnif_train_loss* loss, float* d_grad_mlp, float* d_grad_tables,
+                                      void* stream);
+/* The trainer's own sampler: n labelled samples of training step `step`. */
+lsnif_status lsnif_trainer_sample(lsnif_trainer trainer, int64_t step, int64_t n, lsnif_ray* d_rays,
+                                  lsnif_train_target* d_targets, void* stream);
+
 /* Kernel-level timing of queries (bench / roofline support). When enabled,
  * CUDA events are recorded on the query stream around every kernel launch;
  * lsnif_profile_read synchronises `stream` and returns the summed device

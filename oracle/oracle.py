@@ -75,6 +75,9 @@ def _load(path: str) -> C.CDLL:
     f.oracle_scene_query.argtypes = [_P, _P, C.c_int, _P, C.c_int64, C.c_int, _P, C.c_int]
     f.oracle_render.argtypes = [_P, _P, C.c_int, _P, _P, C.c_int, _P, _P, C.c_int, _P]
     f.oracle_render_debug_paths.argtypes = [_P, C.c_int64, C.c_int64, _P, _P, C.c_int]
+    f.oracle_shape_mesh.argtypes = [C.c_int, _P, _P, _P, _P]
+    f.oracle_label_rays.argtypes = [_P, _P, _P, _P, _P, C.c_int, _P, _P, _P, C.c_int64, _P, _P]
+    f.oracle_train_batch_grad.argtypes = [_P, _P, _P, C.c_int64, _P, _P, _P]
     return lib
 
 
@@ -316,3 +319,54 @@ def render_debug_paths(camera: dict, cfg: dict, first: int, n: int, k: int):
     u = np.zeros((n, max(k, 1)), np.float32)
     _check(L.oracle_render_debug_paths(_ptr(setup), first, n, _ptr(rays), _ptr(u), k), L)
     return rays, u[:, :k]
+
+
+# ---- training (training.cpp, loss.hpp, mlp.hpp backward / Adam)
+
+TARGET_DTYPE = np.dtype([("occluded", "<i4"), ("local_t", "<f4"), ("normal", "<f4", 3),
+                         ("albedo", "<f4", 3), ("material", "<i4")])
+assert TARGET_DTYPE.itemsize == 36
+
+
+def shape_mesh(shape: int):
+    """(verts (nv, 3) f32, faces (nf, 3) i32) of a procedural fixture (shapes.cpp)."""
+    L = lib()
+    nv, nf = C.c_int(), C.c_int()
+    _check(L.oracle_shape_mesh(shape, None, C.byref(nv), None, C.byref(nf)), L)
+    v = np.zeros((nv.value, 3), np.float32)
+    f = np.zeros((nf.value, 3), np.int32)
+    _check(L.oracle_shape_mesh(shape, _ptr(v), C.byref(nv), _ptr(f), C.byref(nf)), L)
+    return v, f
+
+
+def label_rays(mesh: dict, frame, rays: np.ndarray):
+    """label_ray (training.cpp:47-72) per ray -> (targets, ok)."""
+    L = lib()
+    rays = np.ascontiguousarray(rays, RAY_DTYPE)
+    out = np.zeros(len(rays), TARGET_DTYPE)
+    ok = np.zeros(len(rays), np.int8)
+    arr = lambda k, t: (np.ascontiguousarray(mesh[k], t) if mesh.get(k) is not None else None)
+    v, nrm, f, fn, fm = (arr("verts", np.float32), arr("normals", np.float32), arr("faces", np.int32),
+                         arr("face_normals", np.int32), arr("face_material", np.int32))
+    alb = np.ascontiguousarray(mesh["albedo"], np.float32)
+    fr = np.ascontiguousarray(frame, np.float32)
+    p = lambda a: None if a is None else _ptr(a)
+    _check(L.oracle_label_rays(p(v), p(nrm), p(f), p(fn), p(fm), len(f), _ptr(alb), _ptr(fr), _ptr(rays),
+                               len(rays), _ptr(out), _ptr(ok)), L)
+    return out, ok
+
+
+def train_batch_grad(model, rays: np.ndarray, targets: np.ndarray):
+    """(loss[6], grad_mlp, grad_tables) of one batch (training.cpp:161-189)."""
+    L = model.L
+    rays = np.ascontiguousarray(rays, RAY_DTYPE)
+    targets = np.ascontiguousarray(targets, TARGET_DTYPE)
+    K1 = model.H * model.n_levels * model.F
+    hid, n_out = model.hidden, 8 + model.n_mat
+    n_mlp = hid * K1 + hid + hid * hid + hid + n_out * hid + n_out
+    g_mlp = np.zeros(n_mlp, np.float32)
+    g_tab = np.zeros(model.n_levels * model.M * model.F, np.float32)
+    loss = np.zeros(6, np.float32)
+    _check(L.oracle_train_batch_grad(model.h, _ptr(rays), _ptr(targets), len(rays), _ptr(loss), _ptr(g_mlp),
+                                     _ptr(g_tab)), L)
+    return loss, g_mlp, g_tab

@@ -4,6 +4,7 @@
 // thread-local message readable with oracle_last_error().
 #include "lsnif_oracle.hpp"
 #include "lsnif_render_oracle.hpp"
+#include "lsnif_train_oracle.hpp"
 
 #include <chrono>
 #include <cmath>
@@ -406,6 +407,42 @@ int oracle_render(void** models, const float* w2o, int n_inst, const float* setu
 
 int oracle_render_debug_paths(const float* setup, int64_t first, int64_t n, Ray* rays, float* u, int k) {
   return guarded([&] { render_debug_paths(unpack_setup(setup, nullptr, 0, nullptr, 0), first, n, rays, u, k); });
+}
+
+// mesh of a procedural fixture (shape 0 sphere, 1 box, 2 torus): counts first
+// (verts/faces may be NULL), then the arrays.
+int oracle_shape_mesh(int shape, float* verts, int* nv, int* faces, int* nf) {
+  return guarded([&] {
+    ObjMesh mesh;
+    if (shape == 0) mesh = make_uv_sphere(1.0f, 32, 16);
+    else if (shape == 1) {
+      const float h[3] = {1.0f, 0.6f, 0.8f};
+      mesh = make_box(h);
+    } else mesh = make_torus(1.0f, 0.35f, 48, 24);
+    *nv = static_cast<int>(mesh.verts.size() / 3);
+    *nf = static_cast<int>(mesh.faces.size() / 3);
+    if (verts) std::memcpy(verts, mesh.verts.data(), mesh.verts.size() * 4);
+    if (faces) std::memcpy(faces, mesh.faces.data(), mesh.faces.size() * 4);
+  });
+}
+
+int oracle_label_rays(const float* verts, const float* normals, const int* faces, const int* face_normals,
+                      const int* face_material, int n_faces, const float* albedo, const float frame[6],
+                      const Ray* rays, int64_t n, TrainTarget* out, int8_t* ok) {
+  return guarded([&] {
+    TrainMesh M{verts, normals, faces, face_normals, face_material, n_faces, albedo};
+    Aabb box;
+    for (int a = 0; a < 3; ++a) {
+      box.mn[a] = frame[a];
+      box.mx[a] = frame[3 + a];
+    }
+    for (int64_t i = 0; i < n; ++i) ok[i] = label_ray(M, box, rays[i], out[i]) ? 1 : 0;
+  });
+}
+
+int oracle_train_batch_grad(void* mp, const Ray* rays, const TrainTarget* targets, int64_t n, float* loss,
+                            float* g_mlp, float* g_tab) {
+  return guarded([&] { train_batch_grad(*static_cast<Model*>(mp), rays, targets, n, loss, g_mlp, g_tab); });
 }
 
 }  // extern "C"

@@ -761,6 +761,79 @@ lsnif_status lsnif_render_debug_paths(const lsnif_camera* camera, const lsnif_re
   });
 }
 
+struct lsnif_trainer_s {
+  int device = 0;
+  void* impl = nullptr;
+  ~lsnif_trainer_s() {
+    if (impl) lsnif_api::trainer_destroy(impl);
+  }
+};
+
+lsnif_status lsnif_trainer_create(const lsnif_model_desc* init, const lsnif_mesh_desc* mesh,
+                                  const lsnif_train_config* config, int device, lsnif_trainer* out) {
+  return guarded([&] {
+    if (!init || !mesh || !config || !out) fail(LSNIF_INVALID_ARGUMENT, "null trainer argument");
+    lsnif_model geo = nullptr;
+    create_into(*init, device, &geo);  // validates the model, builds the stop mask / frame constants
+    auto T = std::make_unique<lsnif_trainer_s>();
+    T->device = device;
+    try {
+      T->impl = lsnif_api::trainer_create(*init, *mesh, *config, device, geo, geo->dm);
+    } catch (...) {
+      lsnif_model_destroy(geo);
+      throw;
+    }
+    *out = T.release();
+  });
+}
+
+lsnif_status lsnif_trainer_create_from_file(const char* path, const lsnif_mesh_desc* mesh,
+                                            const lsnif_train_config* config, int device, lsnif_trainer* out) {
+  FileModel fm;
+  const lsnif_status st = guarded([&] {
+    if (!path) fail(LSNIF_INVALID_ARGUMENT, "null path");
+    read_model_file(path, fm);
+  });
+  if (st != LSNIF_OK) return st;
+  return lsnif_trainer_create(&fm.desc, mesh, config, device, out);
+}
+
+lsnif_status lsnif_trainer_destroy(lsnif_trainer trainer) {
+  return guarded([&] { delete trainer; });
+}
+
+lsnif_status lsnif_trainer_step(lsnif_trainer trainer, int32_t steps, lsnif_train_loss* last, void* stream) {
+  return guarded([&] {
+    if (!trainer) fail(LSNIF_INVALID_ARGUMENT, "null trainer");
+    lsnif_api::trainer_step(trainer->impl, steps, last, static_cast<cudaStream_t>(stream));
+  });
+}
+
+lsnif_status lsnif_trainer_export(lsnif_trainer trainer, lsnif_model* out) {
+  return guarded([&] {
+    if (!trainer || !out) fail(LSNIF_INVALID_ARGUMENT, "null trainer or output");
+    lsnif_api::trainer_export(trainer->impl, trainer->device, out);
+  });
+}
+
+lsnif_status lsnif_trainer_batch_grad(lsnif_trainer trainer, const lsnif_ray* d_rays,
+                                      const lsnif_train_target* d_targets, int64_t n, lsnif_train_loss* loss,
+                                      float* d_grad_mlp, float* d_grad_tables, void* stream) {
+  return guarded([&] {
+    if (!trainer) fail(LSNIF_INVALID_ARGUMENT, "null trainer");
+    lsnif_api::trainer_batch_grad(trainer->impl, d_rays, d_targets, n, loss, d_grad_mlp, d_grad_tables,
+                                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+lsnif_status lsnif_trainer_sample(lsnif_trainer trainer, int64_t step, int64_t n, lsnif_ray* d_rays,
+                                  lsnif_train_target* d_targets, void* stream) {
+  return guarded([&] {
+    if (!trainer) fail(LSNIF_INVALID_ARGUMENT, "null trainer");
+    lsnif_api::trainer_sample(trainer->impl, step, n, d_rays, d_targets, static_cast<cudaStream_t>(stream));
+  });
+}
+
 const char* lsnif_build_info(void) {
   return "liblsnif_gpu sm_100a: trace_encode_kernel + mlp_tc_kernel (tcgen05 kind::f16, TMEM), "
          "infer_f32_kernel; wavefront renderer (camera/shade/shadow_accum/resolve kernels)";

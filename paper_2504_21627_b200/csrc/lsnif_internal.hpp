@@ -105,3 +105,15 @@ void render(WorkspacePtr& ws, lsnif_scene scene, const float* world_diag, int n_
 void debug_paths(const lsnif_camera& camera, const lsnif_render_config& cfg, int64_t first_path,
                  int64_t n, lsnif_ray* d_rays, float* d_uniforms, int k, cudaStream_t st);
 }  // namespace lsnif_pt
+
+// GPU trainer (lsnif_train.cu), driven by the lsnif_trainer_* entry points.
+namespace lsnif_api {
+void* trainer_create(const lsnif_model_desc& d, const lsnif_mesh_desc& mesh, const lsnif_train_config& cfg,
+                     int device, lsnif_model geo, const lsnif_dev::DevModel& dm);
+void trainer_destroy(void* t);
+void trainer_step(void* t, int steps, lsnif_train_loss* last, cudaStream_t st);
+void trainer_batch_grad(void* t, const lsnif_ray* rays, const lsnif_train_target* tg, int64_t n,
+                        lsnif_train_loss* loss, float* g_mlp, float* g_tab, cudaStream_t st);
+void trainer_sample(void* t, int64_t step, int64_t n, lsnif_ray* rays, lsnif_train_target* tg, cudaStream_t st);
+void trainer_export(void* t, int device, lsnif_model* out);
+}  // namespace lsnif_api

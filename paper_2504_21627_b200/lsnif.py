@@ -87,11 +87,19 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.lsnif_profile_read.argtypes = [P, P, C.c_int, C.POINTER(Profile)]
     lib.lsnif_render.argtypes = [P, P, C.c_int32, P, P, C.c_int32, P, P, P, P, P]
     lib.lsnif_render_debug_paths.argtypes = [P, P, C.c_int64, C.c_int64, P, P, C.c_int32, P]
+    lib.lsnif_trainer_create_from_file.argtypes = [C.c_char_p, P, P, C.c_int, C.POINTER(P)]
+    lib.lsnif_trainer_destroy.argtypes = [P]
+    lib.lsnif_trainer_step.argtypes = [P, C.c_int32, P, P]
+    lib.lsnif_trainer_export.argtypes = [P, C.POINTER(P)]
+    lib.lsnif_trainer_batch_grad.argtypes = [P, P, P, C.c_int64, P, P, P, P]
+    lib.lsnif_trainer_sample.argtypes = [P, C.c_int64, C.c_int64, P, P, P]
     for name in ("lsnif_model_load", "lsnif_model_destroy", "lsnif_model_get_info", "lsnif_query",
                  "lsnif_query_host", "lsnif_infer_batch", "lsnif_debug_traverse",
                  "lsnif_last_query_stats", "lsnif_profile_enable", "lsnif_profile_read",
                  "lsnif_scene_create", "lsnif_scene_destroy", "lsnif_scene_query", "lsnif_render",
-                 "lsnif_render_debug_paths"):
+                 "lsnif_render_debug_paths", "lsnif_trainer_create_from_file", "lsnif_trainer_destroy",
+                 "lsnif_trainer_step", "lsnif_trainer_export", "lsnif_trainer_batch_grad",
+                 "lsnif_trainer_sample"):
         getattr(lib, name).restype = C.c_int
     _lib = lib
     return lib
@@ -366,3 +374,98 @@ def hits_to_numpy(hits) -> np.ndarray:
 def rays_to_tensor(rays: np.ndarray, device="cuda"):
     torch = _torch()
     return torch.from_numpy(np.ascontiguousarray(rays).view(np.float32).reshape(-1, 8).copy()).to(device)
+
+
+# ------------------------------------------------------------ GPU training (F4)
+
+TARGET_DTYPE = np.dtype([("occluded", "<i4"), ("local_t", "<f4"), ("normal", "<f4", 3),
+                         ("albedo", "<f4", 3), ("material", "<i4")])
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [("vertices", C.c_void_p), ("n_vertices", C.c_int32), ("normals", C.c_void_p),
+                ("n_normals", C.c_int32), ("faces", C.c_void_p), ("face_normals", C.c_void_p),
+                ("face_material", C.c_void_p), ("n_faces", C.c_int32)]
+
+
+class TrainConfig(C.Structure):
+    _fields_ = [("batch", C.c_int32), ("lr", C.c_float), ("external_mix", C.c_float),
+                ("seed", C.c_uint64)]
+
+
+class TrainLoss(C.Structure):
+    _fields_ = [("total", C.c_float), ("occlusion_bce", C.c_float), ("local_t_mae", C.c_float),
+                ("normal_cosine", C.c_float), ("albedo_rel_l2", C.c_float), ("material_ce", C.c_float),
+                ("step", C.c_int64)]
+
+
+class _Loaded:  # wraps an exported lsnif_model handle as a GpuModel
+    pass
+
+
+class Trainer:
+    """lsnif::train (training.cpp:95-230) on the GPU: mesh (verts (nv,3),
+    faces (nf,3), optional normals / face_normals, face_material) + a
+    starting LSNF file."""
+
+    def __init__(self, init_path: str, mesh: dict, batch: int = 1 << 14, lr: float = 0.01,
+                 external_mix: float = 0.5, seed: int = 0, device: int = 0):
+        self._keep = {k: (np.ascontiguousarray(v, np.int32 if "face" in k else np.float32)
+                          if v is not None else None) for k, v in mesh.items()}
+        m = self._keep
+        p = lambda a: a.ctypes.data if a is not None else None
+        desc = MeshDesc(p(m["verts"]), len(m["verts"]), p(m.get("normals")),
+                        0 if m.get("normals") is None else len(m["normals"]), p(m["faces"]),
+                        p(m.get("face_normals")), p(m["face_material"]), len(m["faces"]))
+        cfg = TrainConfig(batch, lr, external_mix, seed)
+        h = C.c_void_p()
+        _check(load_library().lsnif_trainer_create_from_file(init_path.encode(), C.byref(desc),
+                                                             C.byref(cfg), device, C.byref(h)))
+        self.h, self.device, self.batch = h, device, batch
+
+    def step(self, steps: int = 1, stream=None) -> dict:
+        loss = TrainLoss()
+        _check(load_library().lsnif_trainer_step(self.h, steps, C.byref(loss), _stream_ptr(stream)))
+        return {k: getattr(loss, k) for k, _ in TrainLoss._fields_}
+
+    def sample(self, step: int, n: int):
+        torch = _torch()
+        rays = torch.empty((n, 8), dtype=torch.float32, device=f"cuda:{self.device}")
+        tg = torch.empty((n, 9), dtype=torch.int32, device=f"cuda:{self.device}")
+        _check(load_library().lsnif_trainer_sample(self.h, step, n, rays.data_ptr(), tg.data_ptr(),
+                                                   _stream_ptr(None)))
+        return rays, tg
+
+    def batch_grad(self, rays, targets, n_mlp: int, n_tab: int):
+        torch = _torch()
+        g_mlp = torch.empty(n_mlp, dtype=torch.float32, device=rays.device)
+        g_tab = torch.empty(n_tab, dtype=torch.float32, device=rays.device)
+        loss = TrainLoss()
+        _check(load_library().lsnif_trainer_batch_grad(self.h, rays.data_ptr(), targets.data_ptr(),
+                                                       rays.shape[0], C.byref(loss), g_mlp.data_ptr(),
+                                                       g_tab.data_ptr(), _stream_ptr(None)))
+        return {k: getattr(loss, k) for k, _ in TrainLoss._fields_}, g_mlp, g_tab
+
+    def export(self) -> "GpuModel":
+        h = C.c_void_p()
+        _check(load_library().lsnif_trainer_export(self.h, C.byref(h)))
+        gm = GpuModel.__new__(GpuModel)
+        gm.h, gm.device = h, self.device
+        info = ModelInfo()
+        _check(load_library().lsnif_model_get_info(gm.h, C.byref(info)))
+        gm.info = info
+        gm.H, gm.n_levels, gm.F = info.hit_cap, info.n_levels, info.f_dim
+        gm.input_width = gm.H * gm.n_levels * gm.F
+        gm.aabb = np.array(list(info.aabb), np.float32)
+        return gm
+
+    def close(self):
+        if getattr(self, "h", None):
+            load_library().lsnif_trainer_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
