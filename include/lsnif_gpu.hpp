@@ -13,6 +13,7 @@
 //                                  occluded_batch over world rays
 //   lsnif::gpu::render           ~ render() (renderer.cpp:453-542),
 //                                  PrimaryMode::lsnif
+//   lsnif::gpu::Trainer          ~ train() (training.cpp:95-230) on the GPU
 // Errors are rethrown as the reference's exception types:
 // std::invalid_argument for LSNIF_INVALID_ARGUMENT, std::runtime_error
 // otherwise.
@@ -74,6 +75,7 @@ class Model {
     check(lsnif_model_create(&desc, device, &m));
     return Model(m);
   }
+  static Model adopt(lsnif_model m) { return Model(m); }  // takes ownership of a C-ABI handle
   lsnif_model handle() const { return h_.get(); }
   lsnif_model_info info() const {
     lsnif_model_info i{};
@@ -218,6 +220,32 @@ inline std::vector<float> render(const Scene& scene, const std::vector<float>& w
   if (px) cudaMemcpy(out.data(), img.ptr, out.size() * sizeof(float), cudaMemcpyDeviceToHost);
   return out;
 }
+
+// train() (training.cpp:95-230): the starting model + the mesh; step() runs
+// optimizer steps on the device, model() exports the binary16 bundle as a
+// query model (save_model + load_model).
+class Trainer {
+ public:
+  Trainer(const lsnif_model_desc& init, const lsnif_mesh_desc& mesh, const lsnif_train_config& cfg,
+          int device = 0) {
+    lsnif_trainer t = nullptr;
+    check(lsnif_trainer_create(&init, &mesh, &cfg, device, &t));
+    h_.reset(t, [](lsnif_trainer p) { lsnif_trainer_destroy(p); });
+  }
+  lsnif_train_loss step(int steps) {
+    lsnif_train_loss loss{};
+    check(lsnif_trainer_step(h_.get(), steps, &loss, nullptr));
+    return loss;
+  }
+  Model model() const {
+    lsnif_model m = nullptr;
+    check(lsnif_trainer_export(h_.get(), &m));
+    return Model::adopt(m);
+  }
+
+ private:
+  std::shared_ptr<lsnif_trainer_s> h_;
+};
 
 }  // namespace gpu
 }  // namespace lsnif
