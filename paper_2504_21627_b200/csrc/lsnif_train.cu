@@ -45,6 +45,7 @@ constexpr int kExternalRetries = 4096; // the reference loops until the ray meet
 // ------------------------------------------------------------- mesh + rng
 
 struct MeshDev {
+  const float4* tri;     // 3 per face: the corner positions (w unused), gathered once
   const float* v;        // 3 per vertex
   const float* n;        // 3 per normal (nullable)
   const int* f;          // 3 per face
@@ -141,27 +142,45 @@ __device__ __forceinline__ bool intersect_triangle(const float o[3], const float
 
 // intersect_closest (bvh.cpp:174-232) over every face: smallest t, ties to
 // the lower face index (a hit at exactly t_max is kept, like the reference).
+// Warp-cooperative: the 32 lanes (which all hold the same ray) test faces
+// lane, lane + 32, ... in increasing order, then reduce (t, face)
+// lexicographically — the same winner as the sequential scan.
 __device__ bool closest_hit(const MeshDev& M, const float o[3], const float d[3], float t_min, float t_max,
                             float& t, float& u, float& v, int& face) {
-  bool found = false;
-  float best = t_max;
-  for (int f = 0; f < M.nf; ++f) {
-    const int i0 = __ldg(M.f + 3 * f), i1 = __ldg(M.f + 3 * f + 1), i2 = __ldg(M.f + 3 * f + 2);
-    const float a[3] = {__ldg(M.v + 3 * i0), __ldg(M.v + 3 * i0 + 1), __ldg(M.v + 3 * i0 + 2)};
-    const float b[3] = {__ldg(M.v + 3 * i1), __ldg(M.v + 3 * i1 + 1), __ldg(M.v + 3 * i1 + 2)};
-    const float c[3] = {__ldg(M.v + 3 * i2), __ldg(M.v + 3 * i2 + 1), __ldg(M.v + 3 * i2 + 2)};
+  const int lane = threadIdx.x & 31;
+  float bt = __int_as_float(0x7f800000), bu = 0.0f, bv = 0.0f;
+  int bf = 0x7fffffff;
+  for (int f = lane; f < M.nf; f += 32) {
+    const float4 A = __ldg(M.tri + 3 * f), B = __ldg(M.tri + 3 * f + 1), Cc = __ldg(M.tri + 3 * f + 2);
+    const float a[3] = {A.x, A.y, A.z}, b[3] = {B.x, B.y, B.z}, c[3] = {Cc.x, Cc.y, Cc.z};
     float th, uh, vh;
     if (!intersect_triangle(o, d, t_min, t_max, a, b, c, th, uh, vh)) continue;
-    if (th < best || (th == best && !found)) {
-      best = th;
-      t = th;
-      u = uh;
-      v = vh;
-      face = f;
-      found = true;
+    if (th < bt || bf == 0x7fffffff) {  // first hit of this lane, or strictly closer
+      bt = th;
+      bu = uh;
+      bv = vh;
+      bf = f;
     }
   }
-  return found;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    const float ot = __shfl_xor_sync(0xffffffffu, bt, off);
+    const int of = __shfl_xor_sync(0xffffffffu, bf, off);
+    const float ou = __shfl_xor_sync(0xffffffffu, bu, off);
+    const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+    if (ot < bt || (ot == bt && of < bf)) {
+      bt = ot;
+      bf = of;
+      bu = ou;
+      bv = ov;
+    }
+  }
+  if (bf == 0x7fffffff) return false;
+  t = bt;
+  u = bu;
+  v = bv;
+  face = bf;
+  return true;
 }
 
 // Mesh::shading_normal (geometry.cpp:58-67) / geometric_normal (35-43)
@@ -275,11 +294,13 @@ __device__ __forceinline__ uint64_t sample_seed(uint64_t seed, uint64_t step, ui
 }
 
 // draw_sample (training.cpp:74-93)
+// One warp per sample: every lane draws the same stream and takes the same
+// path; the triangle scans are split over the lanes (closest_hit).
 __global__ void __launch_bounds__(128) sample_kernel(MeshDev M, Frame fr, uint64_t seed, int64_t step,
                                                      float external_mix, int64_t n, lsnif_ray* rays,
                                                      lsnif_train_target* targets) {
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= n) return;
+  const int64_t j = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (j >= n) return;  // warp-uniform
   Rng rng{sample_seed(seed, static_cast<uint64_t>(step), static_cast<uint64_t>(j))};
   lsnif_train_target tg{};
   float o[3], d[3];
@@ -312,8 +333,10 @@ __global__ void __launch_bounds__(128) sample_kernel(MeshDev M, Frame fr, uint64
   }
   r.t_min = 0.0f;
   r.t_max = __int_as_float(0x7f800000);
-  rays[j] = r;
-  targets[j] = tg;
+  if ((threadIdx.x & 31) == 0) {
+    rays[j] = r;
+    targets[j] = tg;
+  }
 }
 
 // ------------------------------------------------------------- encode
@@ -705,8 +728,8 @@ void read_loss(Trainer& T, cudaStream_t st, lsnif_train_loss* out) {
 }
 
 void sample(Trainer& T, int64_t step, int64_t n, lsnif_ray* rays, lsnif_train_target* tg, cudaStream_t st) {
-  launch(sample_kernel, n, 128, 0, st, "sample_kernel", T.mesh, T.frame, T.cfg.seed, step, T.cfg.external_mix, n,
-         rays, tg);
+  launch(sample_kernel, 32 * n, 128, 0, st, "sample_kernel", T.mesh, T.frame, T.cfg.seed, step,
+         T.cfg.external_mix, n, rays, tg);
 }
 
 }  // namespace lsnif_tr
@@ -777,6 +800,15 @@ void* trainer_create(const lsnif_model_desc& d, const lsnif_mesh_desc& mesh, con
   lsnif_tr::MeshDev& M = T->mesh;
   M.v = T->upload(mesh.vertices, 3 * static_cast<size_t>(mesh.n_vertices));
   M.f = T->upload(mesh.faces, 3 * static_cast<size_t>(mesh.n_faces));
+  {  // corner positions per face, one 16-byte load each in the triangle loop
+    std::vector<float4> tri(3 * static_cast<size_t>(mesh.n_faces));
+    for (int f = 0; f < mesh.n_faces; ++f)
+      for (int k = 0; k < 3; ++k) {
+        const float* p = mesh.vertices + 3 * static_cast<size_t>(mesh.faces[3 * f + k]);
+        tri[3 * static_cast<size_t>(f) + k] = make_float4(p[0], p[1], p[2], 0.0f);
+      }
+    M.tri = T->upload(tri.data(), tri.size());
+  }
   M.fmat = T->upload(mesh.face_material, static_cast<size_t>(mesh.n_faces));
   M.n = nullptr;
   M.fn = nullptr;
