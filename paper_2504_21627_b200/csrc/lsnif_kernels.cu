@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <type_traits>
 
 #include "lsnif_device.cuh"
 #include "lsnif_internal.hpp"
@@ -161,36 +162,19 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
       lane_ray[2 * lane + 1] = make_float4(w.d[0], w.d[1], w.d[2], __int_as_float(bin));
     }
     __syncwarp();
-    // ---- warp-cooperative encode of all pooled points (encoding.hpp:166-176)
-    const int c = valid ? count : 0;
-    int incl = c;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const int v = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += v;
-    }
-    const int excl = incl - c;
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    for (int jb = 0; jb < total; jb += 32) {
-      const int j = jb + lane;
-      int owner = 0;
-#pragma unroll
-      for (int st = 16; st >= 1; st >>= 1) {
-        const int ex = __shfl_sync(0xffffffffu, excl, owner + st);
-        if (ex <= j) owner += st;
-      }
-      const int o_excl = __shfl_sync(0xffffffffu, excl, owner);
-      const int64_t o_ray = wbatch * 32 + owner;
-      if (j >= total) continue;
-      const float4 rq = lane_ray[2 * owner], rr = lane_ray[2 * owner + 1];
-      const float ro[3] = {rq.x, rq.y, rq.z}, rd[3] = {rr.x, rr.y, rr.z};
-      const int o_row = __float_as_int(rq.w);
-      const int o_bin = __float_as_int(rr.w);
-      const int k = j - o_excl;
-      const uint2 e = pool[k * 32 + owner];
+    // ---- warp-cooperative encode of the pooled points (encoding.hpp:166-176):
+    // boundary points in passes of 32 (any lane may take any lane's point),
+    // then the rare inside-origin "volume" first points (8 corners per level)
+    // in one pass of their own, so the boundary passes never diverge into the
+    // volume path.
+    // VOLT: std::integral_constant<bool, volume point> (compile time, so each
+    // pass carries only its own path)
+    auto encode_point = [&](auto VOLT, const float ro[3], const float rd[3], int64_t o_ray, int o_row, int o_bin,
+                            int k, const uint2 e) {
+      constexpr bool volume = decltype(VOLT)::value;
       float p[3];
-      bool volume;
-      unpack_point(e, ro, rd, m.inv_fres, p, volume);
+      bool vol_code;
+      unpack_point(e, ro, rd, m.inv_fres, p, vol_code);
       float fv[16];
       const int pa = volume ? -1 : plane_axis_of(p, m.fres);
       if (LS == 2 && !volume) {
@@ -269,7 +253,35 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
                 __float2half_rn(__fmul_rn(fv[q], scale));
         }
       }
+    };
+    const int vc = (valid && fio) ? 1 : 0;  // this lane's volume point (k = 0)
+    const int c = valid ? count - vc : 0;   // its boundary points (k = vc .. count-1)
+    int incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
     }
+    const int excl = incl - c;
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    for (int jb = 0; jb < total; jb += 32) {
+      const int j = jb + lane;
+      int owner = 0;
+#pragma unroll
+      for (int st = 16; st >= 1; st >>= 1) {
+        const int ex = __shfl_sync(0xffffffffu, excl, owner + st);
+        if (ex <= j) owner += st;
+      }
+      const int o_excl = __shfl_sync(0xffffffffu, excl, owner);
+      const int o_vc = __shfl_sync(0xffffffffu, vc, owner);
+      if (j >= total) continue;
+      const float4 rq = lane_ray[2 * owner], rr = lane_ray[2 * owner + 1];
+      const float ro[3] = {rq.x, rq.y, rq.z}, rd[3] = {rr.x, rr.y, rr.z};
+      const int k = o_vc + j - o_excl;
+      encode_point(std::false_type{}, ro, rd, wbatch * 32 + owner, __float_as_int(rq.w), __float_as_int(rr.w), k,
+                   pool[k * 32 + owner]);
+    }
+    if (vc) encode_point(std::true_type{}, w.o, w.d, ray_idx, row, bin, 0, pool[lane]);
 
     // ---- zero padding of the row tail up to the bin width (encoding.hpp:170)
     if (!DEBUG && valid) {
