@@ -108,6 +108,48 @@ def load_traffic(workload: str):
         return {}
 
 
+def load_json(name: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def aux_rooflines(workload: str, trace_rays_per_s: float, sm_mhz, pts_per_ray: float, vol_per_ray: float):
+    """The trace kernel is SIMT-issue bound (SURVEY §8(d) 'auxiliary issue
+    ceiling'): warp instructions per ray from the committed ncu capture x the
+    live rays/s, against 148 SMs x 4 issue slots x the measured clock; and its
+    hash-table gathers (8 per boundary point, 16 per volume point) against the
+    measured L2 random 8-byte gather rate (scripts/micro/l2_bw.cu)."""
+    km = load_json(f"kernel_metrics_{workload}.json").get("trace_encode_kernel")
+    out = {}
+    clk = (sm_mhz or 1965.0) * 1e6
+    if km:
+        ach = km["warp_inst_per_ray"] * trace_rays_per_s
+        peak = 148 * 4 * clk
+        out["roofline_issue"] = {
+            "kernel": "trace_encode_kernel", "bound": "issue", "achieved": ach, "peak": peak,
+            "unit": "warp-inst/s", "frac": ach / peak, "ncu_issue_active": km["issue_active_frac"],
+            "source": f"profiles/kernel_metrics_{workload}.json ({km['warp_inst_per_ray']:.1f} warp-inst/ray, "
+                      "ncu) x live trace rays/s; peak = 148 SMs x 4 schedulers x SM clock"}
+    l2 = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "micro", "r1s2_l2_bw.jsonl")) as f:
+            l2 = json.loads(f.readline())
+    except Exception:
+        pass
+    if l2:
+        g = (8.0 * pts_per_ray + 8.0 * vol_per_ray) * trace_rays_per_s
+        peak = l2["gather8_Gloads_per_s"] * 1e9
+        out["l2_gather"] = {"kernel": "trace_encode_kernel", "achieved": g, "peak": peak, "unit": "gathers/s",
+                            "frac": g / peak, "gather_bytes": 8,
+                            "source": "8-byte hash-table entry loads per boundary point (2 levels x 4 "
+                                      "corners, +8 per volume point) x live rays/s; peak = measured L2 random "
+                                      "8-byte gather rate (profiles/micro/r1s2_l2_bw.jsonl)"}
+    return out
+
+
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
@@ -602,6 +644,8 @@ def main():
             "gpu_launches": prof["launches"],
             "clocks": clocks.summary(),
         }
+        line.update(aux_rooflines(args.workload, n_step / (tr_ms / 1e3) if tr_ms > 0 else 0.0,
+                                  line["clocks"].get("sm_mhz"), pts / n_step, vol / n_step))
         if world == 1 and not args.no_cpu_baseline:
             try:
                 O = cpu_oracle(True)
