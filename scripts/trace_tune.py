@@ -35,14 +35,22 @@ for lib in libs:
                 gm.query(d, mode, out=out)
             gm.profile_read(reset=True)
             reps = 10
+            tot = 0.0
             for _ in range(reps):
                 flush.add_(1)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
                 gm.query(d, mode, out=out)
+                e1.record()
+                torch.cuda.synchronize()
+                tot += e0.elapsed_time(e1)
             p = gm.profile_read(reset=True)
             gm.profile_enable(False)
             r = dict(lib=os.path.basename(lib), drain=int(dr), set=name, rays=d.shape[0],
                      trace_ms=p["trace_ms"] / reps, mlp_ms=p["mlp_ms"] / reps)
             r["grays_s_trace"] = d.shape[0] / r["trace_ms"] / 1e6
+            r["query_ms"] = tot / reps
+            r["sort"] = os.environ.get("LSNIF_TRACE_SORT", "1")
             r["stats"] = st
             res.append(r)
             print(json.dumps(r), flush=True)
