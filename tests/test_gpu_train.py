@@ -98,3 +98,23 @@ def test_training_reduces_loss_and_improves_queries(setup):
     before = occlusion_accuracy(lsnif.GpuModel(INIT), rays, tg)
     after = occlusion_accuracy(tr.export(), rays, tg)
     assert after > before + 0.2 and after > 0.9, (before, after)
+
+
+def test_box_labels_geometric_normals(setup):
+    """A mesh without vertex normals (the box fixture): geometric normals,
+    ray/box edge cases; labels bit-exact against the oracle."""
+    O, _, _ = setup
+    verts, faces = O.shape_mesh(1)
+    mesh = dict(verts=verts, faces=faces, face_material=np.zeros(len(faces), np.int32))
+    init = os.path.join(GOLD, "box_seed3.lsnif")
+    tr = lsnif.Trainer(init, mesh, batch=1024, seed=11)
+    rays, tg = tr.sample(step=7, n=8192)
+    got = targets_np(tg)
+    ref, ok = O.label_rays(dict(mesh, albedo=np.full(3, 0.7, np.float32)), O.OracleModel.load(init).aabb,
+                           rays.cpu().numpy().view(O.RAY_DTYPE).reshape(-1))
+    assert ok.all()
+    for f in ("occluded", "local_t", "normal", "albedo", "material"):
+        assert np.array_equal(got[f], ref[f]), f
+    occ = got["occluded"] != 0
+    n = got["normal"][occ]
+    assert np.allclose(np.abs(n).max(axis=1), 1.0)  # box normals are axis-aligned
