@@ -139,6 +139,12 @@ def aux_rooflines(workload: str, trace_rays_per_s: float, sm_mhz, pts_per_ray: f
             l2 = json.loads(f.readline())
     except Exception:
         pass
+    if l2 and km:
+        rd = km["l2_read_bytes_per_ray"] * trace_rays_per_s / 1e9
+        out["l2_read"] = {"kernel": "trace_encode_kernel", "achieved": rd, "peak": l2["l2_stream_read_GBps"],
+                          "unit": "GB/s", "frac": rd / l2["l2_stream_read_GBps"],
+                          "source": "ncu L2 read sectors per ray (rays, tables, occupancy) x live rays/s; "
+                                    "peak = measured streaming L2 read bandwidth"}
     if l2:
         g = (8.0 * pts_per_ray + 8.0 * vol_per_ray) * trace_rays_per_s
         peak = l2["gather8_Gloads_per_s"] * 1e9
