@@ -629,11 +629,12 @@ struct lsnif_scene_s {
   int device = 0;
   std::vector<lsnif_model> models;
   std::vector<lsnif_dev::InstanceParams> inst;
+  lsnif_dev::InstanceBox* boxes = nullptr;  // device: per-instance transform + frame box
   struct Scratch {
-    lsnif_ray* orays = nullptr;
+    lsnif_ray* orays = nullptr;   // instance k's pairs at k * cap
     int32_t* slots = nullptr;
-    lsnif_hit* hits = nullptr;
-    int32_t* count = nullptr;
+    lsnif_hit* hits = nullptr;    // one instance at a time
+    int32_t* count = nullptr;     // per instance
     int64_t cap = 0;
     ~Scratch() {
       cudaFree(orays);
@@ -647,12 +648,15 @@ struct lsnif_scene_s {
   std::mutex render_mu;
   std::map<cudaStream_t, lsnif_pt::WorkspacePtr> render_ws;  // renderer path state per stream
 
+  ~lsnif_scene_s() { cudaFree(boxes); }
+
   Scratch& get(cudaStream_t st, int64_t n) {
     std::lock_guard<std::mutex> lock(mu);
     auto& s = scratch[st];
+    const size_t ni = std::max<size_t>(inst.size(), 1);
     if (!s) {
       s = std::make_unique<Scratch>();
-      ck(cudaMalloc(&s->count, 64), "cudaMalloc(scene count)");
+      ck(cudaMalloc(&s->count, ni * sizeof(int32_t)), "cudaMalloc(scene count)");
     }
     if (n > s->cap) {
       cudaFree(s->orays);
@@ -661,8 +665,8 @@ struct lsnif_scene_s {
       s->orays = nullptr;
       s->slots = nullptr;
       s->hits = nullptr;
-      ck(cudaMalloc(&s->orays, n * sizeof(lsnif_ray)), "cudaMalloc(scene rays)");
-      ck(cudaMalloc(&s->slots, n * sizeof(int32_t)), "cudaMalloc(scene slots)");
+      ck(cudaMalloc(&s->orays, ni * n * sizeof(lsnif_ray)), "cudaMalloc(scene rays)");
+      ck(cudaMalloc(&s->slots, ni * n * sizeof(int32_t)), "cudaMalloc(scene slots)");
       ck(cudaMalloc(&s->hits, n * sizeof(lsnif_hit)), "cudaMalloc(scene hits)");
       s->cap = n;
     }
@@ -682,14 +686,21 @@ void scene_query_async(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n, co
   if (n == 0) return;
   ck(cudaSetDevice(scene->device), "cudaSetDevice");
   auto& S = scene->get(st, n);
-  ck(lsnif_dev::launch_scene_init(d_rays, n, d_n, d_hits, st), "scene_init_kernel");
-  for (size_t k = 0; k < scene->inst.size(); ++k) {  // object order (renderer.cpp:175-179)
+  const int ni = static_cast<int>(scene->inst.size());
+  if (ni == 0) {
+    ck(lsnif_dev::launch_scene_init(d_rays, n, d_n, d_hits, st), "scene_init_kernel");
+    return;
+  }
+  // one pass over the rays: scene hits initialised + every instance's pairs
+  ck(cudaMemsetAsync(S.count, 0, ni * sizeof(int32_t), st), "cudaMemsetAsync");
+  ck(lsnif_dev::launch_broad_phase_all(scene->boxes, ni, d_rays, n, d_n, S.orays, S.slots, S.cap, S.count, d_hits,
+                                       st),
+     "broad_phase_all_kernel");
+  for (int k = 0; k < ni; ++k) {  // object order (renderer.cpp:175-179)
     lsnif_model_s& M = *scene->models[k];
-    ck(cudaMemsetAsync(S.count, 0, 4, st), "cudaMemsetAsync");
-    ck(lsnif_dev::launch_broad_phase(M.dm, scene->inst[k], d_rays, n, d_n, S.orays, S.slots, S.count, st),
-       "broad_phase_kernel");
-    run_query(M, S.orays, n, mode, S.hits, st, S.count);
-    ck(lsnif_dev::launch_merge(M.dm, scene->inst[k], d_rays, S.hits, S.slots, S.count, n, mode, d_hits, st),
+    run_query(M, S.orays + k * S.cap, n, mode, S.hits, st, S.count + k);
+    ck(lsnif_dev::launch_merge(M.dm, scene->inst[k], d_rays, S.hits, S.slots + k * S.cap, S.count + k, n, mode,
+                               d_hits, st),
        "merge_kernel");
   }
 }
@@ -716,6 +727,20 @@ lsnif_status lsnif_scene_create(const lsnif_instance* instances, int32_t n, lsni
       S->inst.push_back(ip);
     }
     S->device = n > 0 ? instances[0].model->device : 0;
+    if (n > 0) {
+      std::vector<lsnif_dev::InstanceBox> boxes(static_cast<size_t>(n));
+      for (int32_t k = 0; k < n; ++k) {
+        std::memcpy(boxes[k].w2o, instances[k].world_to_object, sizeof(boxes[k].w2o));
+        for (int a = 0; a < 3; ++a) {
+          boxes[k].mn[a] = instances[k].model->dm.mn[a];
+          boxes[k].mx[a] = instances[k].model->dm.mx[a];
+        }
+      }
+      ck(cudaSetDevice(S->device), "cudaSetDevice");
+      ck(cudaMalloc(&S->boxes, boxes.size() * sizeof(lsnif_dev::InstanceBox)), "cudaMalloc(scene boxes)");
+      ck(cudaMemcpy(S->boxes, boxes.data(), boxes.size() * sizeof(lsnif_dev::InstanceBox), cudaMemcpyHostToDevice),
+         "cudaMemcpy(scene boxes)");
+    }
     *out = S.release();
   });
 }

@@ -66,6 +66,19 @@ struct InstanceParams {
   int32_t index;
 };
 
+// One instance's broad-phase data (device array, one entry per instance).
+struct InstanceBox {
+  float w2o[12];
+  float mn[3], mx[3];  // the model's frame box
+};
+
+// collect_pairs for every instance in one pass over the rays (scene_init
+// fused): instance k's object-space rays / slots at orays / slots + k * stride,
+// its pair count at counts[k].
+cudaError_t launch_broad_phase_all(const InstanceBox* boxes, int n_inst, const lsnif_ray* rays, int64_t n,
+                                   const int32_t* n_dev, lsnif_ray* orays, int32_t* slots, int64_t stride,
+                                   int32_t* counts, lsnif_scene_hit* out, cudaStream_t st);
+
 size_t trace_smem_bytes(const DevModel& m);
 cudaError_t compute_zero_hit(const DevModel& m, lsnif_hit* host_out);  // decode of z_zero, enter 0, exit 1
 // n_dev (nullable): device-side ray count, n its upper bound

@@ -750,6 +750,91 @@ __global__ void __launch_bounds__(256) broad_phase_kernel(const DevModel m, cons
   }
 }
 
+// collect_pairs (renderer.cpp:154-181) for all instances in one pass: each
+// ray is read once, its scene hit initialised (scene_init_kernel), and every
+// instance whose frame box it meets before t_max gets the object-space ray
+// appended to its own pair list (warp-aggregated per instance).
+__global__ void __launch_bounds__(256) broad_phase_all_kernel(const InstanceBox* __restrict__ boxes, int n_inst,
+                                                              const lsnif_ray* __restrict__ rays, int64_t n,
+                                                              const int32_t* n_dev, lsnif_ray* __restrict__ orays,
+                                                              int32_t* __restrict__ slots, int64_t stride,
+                                                              int32_t* counts, lsnif_scene_hit* out) {
+  if (n_dev) n = min(n, static_cast<int64_t>(*n_dev));
+  if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= n) return;  // whole block past the count
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool live = i < n;
+  float p[3] = {0, 0, 0}, d[3] = {0, 0, 0}, t_min = 0.f, t_max = 0.f;
+  if (live) {
+    const float4* r4 = reinterpret_cast<const float4*>(rays + i);
+    const float4 a = __ldg(r4), b = __ldg(r4 + 1);
+    p[0] = a.x;
+    p[1] = a.y;
+    p[2] = a.z;
+    d[0] = a.w;
+    d[1] = b.x;
+    d[2] = b.y;
+    t_min = b.z;
+    t_max = b.w;
+    float4* o = reinterpret_cast<float4*>(out + i);  // best_t = t_max, no hit (renderer.cpp:275)
+    o[0] = make_float4(t_max, 0.f, 0.f, 0.f);
+    o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    o[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+    o[3] = make_float4(__int_as_float(-1), 0.f, 0.f, 0.f);
+  }
+  for (int k = 0; k < n_inst; ++k) {
+    const InstanceBox& B = boxes[k];
+    float op[3], od[3];
+    bool keep = false;
+    if (live) {
+      to_object(B.w2o, p, d, op, od);
+      // ray_aabb_intersect on the frame box, t_max = inf; kept iff enter < t_max
+      float t0 = t_min, t1 = __int_as_float(0x7f800000);
+      keep = true;
+#pragma unroll
+      for (int a = 0; a < 3 && keep; ++a) {
+        if (od[a] == 0.0f) {
+          if (op[a] < B.mn[a] || op[a] > B.mx[a]) keep = false;
+          continue;
+        }
+        const float inv = __frcp_rn(od[a]);
+        float ta = __fmul_rn(__fsub_rn(B.mn[a], op[a]), inv);
+        float tb = __fmul_rn(__fsub_rn(B.mx[a], op[a]), inv);
+        if (ta > tb) {
+          const float x = ta;
+          ta = tb;
+          tb = x;
+        }
+        t0 = smax(t0, ta);
+        t1 = smin(t1, tb);
+        if (t0 > t1) keep = false;
+      }
+      keep = keep && t0 < t_max;
+    }
+    const unsigned mask = __ballot_sync(0xffffffffu, keep);
+    if (!mask) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(counts + k, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (keep) {
+      const int64_t j = static_cast<int64_t>(k) * stride + base + __popc(mask & ((1u << lane) - 1u));
+      float4* dst = reinterpret_cast<float4*>(orays + j);
+      dst[0] = make_float4(op[0], op[1], op[2], od[0]);
+      dst[1] = make_float4(od[1], od[2], t_min, t_max);
+      slots[j] = static_cast<int32_t>(i);
+    }
+  }
+}
+
+cudaError_t launch_broad_phase_all(const InstanceBox* boxes, int n_inst, const lsnif_ray* rays, int64_t n,
+                                   const int32_t* n_dev, lsnif_ray* orays, int32_t* slots, int64_t stride,
+                                   int32_t* counts, lsnif_scene_hit* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  broad_phase_all_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(boxes, n_inst, rays, n, n_dev, orays,
+                                                                                slots, stride, counts, out);
+  return cudaGetLastError();
+}
+
 // Accept + merge of one instance's neural hits into the scene result, in
 // object order (renderer.cpp:280-301 closest, 316-321 any): each ray occurs
 // at most once per instance list, so no atomics are needed.
