@@ -630,10 +630,17 @@ struct lsnif_scene_s {
   std::vector<lsnif_model> models;
   std::vector<lsnif_dev::InstanceParams> inst;
   lsnif_dev::InstanceBox* boxes = nullptr;  // device: per-instance transform + frame box
+  // Per-instance narrow phases run concurrently on side streams (fork/join
+  // with events around them; the merges stay in object order on the caller's
+  // stream). The enqueue section is serialised by side_mu.
+  std::mutex side_mu;
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> side_done;
+  cudaEvent_t fork = nullptr;
   struct Scratch {
     lsnif_ray* orays = nullptr;   // instance k's pairs at k * cap
     int32_t* slots = nullptr;
-    lsnif_hit* hits = nullptr;    // one instance at a time
+    lsnif_hit* hits = nullptr;    // instance k's results at k * cap
     int32_t* count = nullptr;     // per instance
     int64_t cap = 0;
     ~Scratch() {
@@ -648,7 +655,12 @@ struct lsnif_scene_s {
   std::mutex render_mu;
   std::map<cudaStream_t, lsnif_pt::WorkspacePtr> render_ws;  // renderer path state per stream
 
-  ~lsnif_scene_s() { cudaFree(boxes); }
+  ~lsnif_scene_s() {
+    cudaFree(boxes);
+    for (cudaStream_t x : side) cudaStreamDestroy(x);
+    for (cudaEvent_t e : side_done) cudaEventDestroy(e);
+    if (fork) cudaEventDestroy(fork);
+  }
 
   Scratch& get(cudaStream_t st, int64_t n) {
     std::lock_guard<std::mutex> lock(mu);
@@ -667,7 +679,7 @@ struct lsnif_scene_s {
       s->hits = nullptr;
       ck(cudaMalloc(&s->orays, ni * n * sizeof(lsnif_ray)), "cudaMalloc(scene rays)");
       ck(cudaMalloc(&s->slots, ni * n * sizeof(int32_t)), "cudaMalloc(scene slots)");
-      ck(cudaMalloc(&s->hits, n * sizeof(lsnif_hit)), "cudaMalloc(scene hits)");
+      ck(cudaMalloc(&s->hits, ni * n * sizeof(lsnif_hit)), "cudaMalloc(scene hits)");
       s->cap = n;
     }
     return *s;
@@ -696,13 +708,32 @@ void scene_query_async(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n, co
   ck(lsnif_dev::launch_broad_phase_all(scene->boxes, ni, d_rays, n, d_n, S.orays, S.slots, S.cap, S.count, d_hits,
                                        st),
      "broad_phase_all_kernel");
-  for (int k = 0; k < ni; ++k) {  // object order (renderer.cpp:175-179)
-    lsnif_model_s& M = *scene->models[k];
-    run_query(M, S.orays + k * S.cap, n, mode, S.hits, st, S.count + k);
-    ck(lsnif_dev::launch_merge(M.dm, scene->inst[k], d_rays, S.hits, S.slots + k * S.cap, S.count + k, n, mode,
-                               d_hits, st),
-       "merge_kernel");
+  // narrow phases: independent per instance, concurrently on side streams
+  constexpr int kMaxSide = 8;
+  std::lock_guard<std::mutex> lock(scene->side_mu);
+  const int nside = std::min(ni, kMaxSide);
+  while (static_cast<int>(scene->side.size()) < nside) {
+    cudaStream_t x;
+    cudaEvent_t e;
+    ck(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    scene->side.push_back(x);
+    scene->side_done.push_back(e);
   }
+  if (!scene->fork) ck(cudaEventCreateWithFlags(&scene->fork, cudaEventDisableTiming), "cudaEventCreate");
+  ck(cudaEventRecord(scene->fork, st), "cudaEventRecord");
+  for (int q = 0; q < nside; ++q) ck(cudaStreamWaitEvent(scene->side[q], scene->fork, 0), "cudaStreamWaitEvent");
+  for (int k = 0; k < ni; ++k)
+    run_query(*scene->models[k], S.orays + k * S.cap, n, mode, S.hits + k * S.cap, scene->side[k % nside],
+              S.count + k);
+  for (int q = 0; q < nside; ++q) {
+    ck(cudaEventRecord(scene->side_done[q], scene->side[q]), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(st, scene->side_done[q], 0), "cudaStreamWaitEvent");
+  }
+  for (int k = 0; k < ni; ++k)  // merges in object order (renderer.cpp:175-179)
+    ck(lsnif_dev::launch_merge(scene->models[k]->dm, scene->inst[k], d_rays, S.hits + k * S.cap,
+                               S.slots + k * S.cap, S.count + k, n, mode, d_hits, st),
+       "merge_kernel");
 }
 
 }  // namespace lsnif_api
