@@ -40,6 +40,9 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
   const int H = m.H;
   const int V = VS ? VS : m.V;
   const int occ_words = m.stop_words;
+  // the MLP kernel (launched as a programmatic dependent) may start its
+  // prologue while this grid runs; it waits for our completion before reading
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.stop + i);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -414,40 +417,11 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   constexpr int kZSlots = 10;          // logits a thread keeps for its deferred decode
   float* zslots = reinterpret_cast<float*>(sX + NS * xstage + 1024);  // 16 warps x 10 x 32
 
-  // tiles of all K bins, bin-major: global tile -> (bin b, tile t within b)
-  const int nb = m.n_bins;
-  int ntiles = 0;
-  for (int b = 0; b < nb; ++b) ntiles += (P.row_counter[b] + kTileM - 1) / kTileM;
-  if (static_cast<int>(blockIdx.x) >= ntiles) return;
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int b = 0; b < nb; ++b) {
-      tstart[b] = acc;
-      acc += (P.row_counter[b] + kTileM - 1) / kTileM;
-    }
-    tstart[nb] = acc;
-    for (int b = 0; b < nb; ++b) bin_rows_n[b] = P.row_counter[b];
-  }
-  // constant A slab of layer 1's bias K-step: column 0 = act_scale, 128 rows
-  // (W1's last 16-column slab holds b1 in column 0)
-  for (int r = threadIdx.x; r < kTileM; r += blockDim.x) {
-    const uint32_t hs = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(m.act_scale)));
-    *reinterpret_cast<uint4*>(sC + canon_offset(r, 0, kTileM)) = make_uint4(hs, 0u, 0u, 0u);
-    *reinterpret_cast<uint4*>(sC + canon_offset(r, 8, kTileM)) = make_uint4(0u, 0u, 0u, 0u);
-  }
-  tc::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
-  auto locate = [&](int tile, int& b, int& t) {
-    b = 0;
-    while (tile >= tstart[b + 1]) ++b;
-    t = tile - tstart[b];
-  };
-  const int64_t bin_rows = P.cap_tiles * kTileM;
-  const int my_tiles = (ntiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
-                       static_cast<int>(gridDim.x);
-
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
+  // ---- prologue, independent of the trace kernel's results: with
+  // programmatic dependent launch it overlaps the trace kernel's tail
   if (tid == 0) {
     tc::mbar_init(w_full, 1);
     for (int s = 0; s < NS; ++s) {
@@ -461,19 +435,62 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     }
     tc::fence_mbar_init();
   }
+  // constant A slab of layer 1's bias K-step: column 0 = act_scale, 128 rows
+  // (W1's last 16-column slab holds b1 in column 0)
+  for (int r = threadIdx.x; r < kTileM; r += blockDim.x) {
+    const uint32_t hs = static_cast<uint32_t>(__half_as_ushort(__float2half_rn(m.act_scale)));
+    *reinterpret_cast<uint4*>(sC + canon_offset(r, 0, kTileM)) = make_uint4(hs, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(sC + canon_offset(r, 8, kTileM)) = make_uint4(0u, 0u, 0u, 0u);
+  }
+  tc::fence_proxy_async_smem();  // generic-proxy writes -> visible to the tensor core
   if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * Lay::kGroupCols);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tid == 0) {  // the weights stay in SMEM for the kernel's lifetime
+    tc::mbar_arrive_expect_tx(w_full, m.w1_bytes + m.w2_bytes + m.w3_bytes);
+    tc::bulk_g2s(sW1, m.w_canon, m.w1_bytes, w_full);
+    tc::bulk_g2s(sW2, m.w_canon + m.w1_bytes, m.w2_bytes, w_full);
+    tc::bulk_g2s(sW3, m.w_canon + m.w1_bytes + m.w2_bytes, m.w3_bytes, w_full);
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the trace kernel's rows are complete
+
+  // tiles of all K bins, bin-major: global tile -> (bin b, tile t within b)
+  const int nb = m.n_bins;
+  int ntiles = 0;
+  for (int b = 0; b < nb; ++b) ntiles += (P.row_counter[b] + kTileM - 1) / kTileM;
+  if (static_cast<int>(blockIdx.x) >= ntiles) {  // nothing to do: release what the prologue took
+    if (tid == 0) tc::mbar_wait(w_full, 0);
+    __syncthreads();
+    if (warp == 1) {
+      tc::tc_fence_after();
+      tc::tmem_dealloc(tmem, 2 * Lay::kGroupCols);
+    }
+    return;
+  }
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      tstart[b] = acc;
+      acc += (P.row_counter[b] + kTileM - 1) / kTileM;
+    }
+    tstart[nb] = acc;
+    for (int b = 0; b < nb; ++b) bin_rows_n[b] = P.row_counter[b];
+  }
+  __syncthreads();
+  auto locate = [&](int tile, int& b, int& t) {
+    b = 0;
+    while (tile >= tstart[b + 1]) ++b;
+    t = tile - tstart[b];
+  };
+  const int64_t bin_rows = P.cap_tiles * kTileM;
+  const int my_tiles = (ntiles - static_cast<int>(blockIdx.x) + static_cast<int>(gridDim.x) - 1) /
+                       static_cast<int>(gridDim.x);
 
   if (warp == 0) {
     // ------------------------------------------------------------ loader
     if (lane == 0) {
-      tc::mbar_arrive_expect_tx(w_full, m.w1_bytes + m.w2_bytes + m.w3_bytes);
-      tc::bulk_g2s(sW1, m.w_canon, m.w1_bytes, w_full);
-      tc::bulk_g2s(sW2, m.w_canon + m.w1_bytes, m.w2_bytes, w_full);
-      tc::bulk_g2s(sW3, m.w_canon + m.w1_bytes + m.w2_bytes, m.w3_bytes, w_full);
       constexpr int kPrefetch = 8;
       auto tile_src = [&](int i, uint32_t& bytes) -> const uint8_t* {
         int b, t;
@@ -1039,8 +1056,17 @@ cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStrea
     c.dev = dev;
     c.smem = smem;
   }
-  mlp_tc_kernel<128><<<grid, MlpLayout<128>::kThreads, smem, st>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(MlpLayout<128>::kThreads);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // programmatic dependent launch
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  return cudaLaunchKernelEx(&lc, mlp_tc_kernel<128>, p);
 }
 
 cudaError_t launch_infer_f32(const DevModel& m, const float* x, int64_t n, const lsnif_interval* iv,
