@@ -108,14 +108,23 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
       if (count < H) {
         while (walk_step(w, tn, p1, p2)) {
           if (stop_bit(smem, w.idx)) {
-            int c[3];
-            walk_cell<VS>(m, w.idx, c);
+            // The crossed plane of the stepped axis (dda.cpp:89-95: c_new for
+            // +steps, c_new + 1 for -steps) is the integer nearest to
+            // V * (o + tn d) along that axis: tn is within a few ulps of the
+            // exact crossing, far below half a cell. Crossing plane V going
+            // up / plane 0 going down means the set bit is the border: the
+            // walk left the grid (dda.cpp:112).
             const int axis = p2 ? 2 : (p1 ? 1 : 0);
-            const int ca = axis == 0 ? c[0] : axis == 1 ? c[1] : c[2];
-            if (ca < 0 || ca >= V) break;  // left the grid (dda.cpp:112)
-            const float da = axis == 0 ? w.d[0] : axis == 1 ? w.d[1] : w.d[2];
-            pool[count * 32 + lane] = pack_point(tn, axis, static_cast<float>(da > 0.0f ? ca : ca + 1));
-            if (DEBUG) P.cells[ray_idx * H + count] = c[0] | c[1] << 8 | c[2] << 16;
+            const float oa = p2 ? w.o[2] : (p1 ? w.o[1] : w.o[0]);
+            const float da = p2 ? w.d[2] : (p1 ? w.d[1] : w.d[0]);
+            const int plane = static_cast<int>(rintf(__fmul_rn(__fadd_rn(oa, __fmul_rn(tn, da)), m.fres)));
+            if (plane == (da > 0.0f ? V : 0)) break;
+            pool[count * 32 + lane] = pack_point(tn, axis, static_cast<float>(plane));
+            if (DEBUG) {
+              int c[3];
+              walk_cell<VS>(m, w.idx, c);
+              P.cells[ray_idx * H + count] = c[0] | c[1] << 8 | c[2] << 16;
+            }
             if (++count >= H) break;  // first-H truncation (dda.cpp:99)
           }
         }
