@@ -84,3 +84,23 @@ def test_shadow_rays_point_at_light():
     assert len(rays) == len(owner) and np.all(owner % 3 == 0)
     p_end = rays["o"] + rays["t_max"][:, None] / (1 - 1e-4) * rays["d"]
     assert np.allclose(p_end, W.LIGHT, atol=1e-3)
+
+
+def test_render_and_trainer_fail_loudly_without_gpu_work(tmp_path):
+    """Argument checks of the F3/F4 entry points run before any device work."""
+    lib = lsnif.load_library()
+    cfg = lsnif._config(dict(width=8, height=8, spp=1, max_bounces=1))
+    cam = lsnif._camera(W.RENDER_CAMERA)
+    assert lib.lsnif_render(None, None, 0, ctypes.byref(cam), None, 0, None, ctypes.byref(cfg), None, None,
+                            None) == lsnif.INVALID_ARGUMENT
+    assert b"null scene" in lib.lsnif_last_error()
+    bad = lsnif._config(dict(width=0, height=8, spp=1, max_bounces=1))
+    assert lib.lsnif_render_debug_paths(ctypes.byref(cam), ctypes.byref(bad), 0, 4, None, None, 0,
+                                        None) == lsnif.INVALID_ARGUMENT
+    h = ctypes.c_void_p()
+    mesh = lsnif.MeshDesc()
+    tc = lsnif.TrainConfig(1024, 0.01, 0.5, 0)
+    st = lib.lsnif_trainer_create_from_file(str(tmp_path / "missing.lsnif").encode(), ctypes.byref(mesh),
+                                            ctypes.byref(tc), 0, ctypes.byref(h))
+    assert st == lsnif.RUNTIME_ERROR and b"cannot open model file" in lib.lsnif_last_error()
+    assert lib.lsnif_trainer_step(None, 1, None, None) == lsnif.INVALID_ARGUMENT
