@@ -225,12 +225,13 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
   if (H > lsnif_dev::kMaxHitCap) fail(LSNIF_UNSUPPORTED, "hit cap > 32 is not supported");
   if (L > lsnif_dev::kMaxLevels || F > 4 || L * F > 16)
     fail(LSNIF_UNSUPPORTED, "need n_levels <= 4, f_dim <= 4, n_levels * f_dim <= 16");
-  if (hid != 128) fail(LSNIF_UNSUPPORTED, "hidden width must be 128 (the paper's high-quality LSNIF)");
+  if (hid != 128 && hid != 64)
+    fail(LSNIF_UNSUPPORTED, "hidden width must be 128 or 64 (the paper's high- / low-quality LSNIF)");
   const int n_out = 8 + d.n_mat;
   if (n_out > 16) fail(LSNIF_UNSUPPORTED, "n_mat > 8 is not supported");
   const int K1 = H * L * F;
   const int K1P = (K1 + 15) / 16 * 16;
-  if (K1P > hid + 16) fail(LSNIF_UNSUPPORTED, "input width H*L*F must be <= hidden + 16");
+
   if (K1P / 16 > lsnif_dev::kMaxBins) fail(LSNIF_UNSUPPORTED, "input width H*L*F must be <= 256");
 
   DevModel& m = M.dm;

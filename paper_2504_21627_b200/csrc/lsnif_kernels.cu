@@ -343,8 +343,8 @@ struct MlpLayout {
   static constexpr int kEpiWarps = 8;         // per group
   static constexpr int kThreads = 32 * (2 + 2 * kEpiWarps);
   static constexpr int kXStages = 4;
-  static constexpr uint32_t kGroupCols = 256; // TMEM columns per group (D + A_h)
-  static constexpr uint32_t kACol = 128;      // A_h column offset within a group
+  static constexpr uint32_t kGroupCols = HID == 128 ? 256 : 128;  // TMEM columns per group (D + A_h)
+  static constexpr uint32_t kACol = HID;      // A_h column offset within a group
 };
 
 __device__ __forceinline__ uint32_t leaky_pack(uint32_t a, uint32_t b) {
@@ -355,20 +355,27 @@ __device__ __forceinline__ uint32_t leaky_pack(uint32_t a, uint32_t b) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// h = leaky(D) for hidden columns [c0, c0 + 64) of this lane's row -> packed
-// fp16 pairs in A_h columns [c0/2, c0/2 + 32). The bias is already in D (a
-// constant-operand K-step) and the activation scale carries through the
-// positively homogeneous leaky-ReLU.
-__device__ __forceinline__ void epi_hidden64(uint32_t tD, uint32_t tA, int c0) {
+// h = leaky(D) for hidden columns [c0, c0 + NC) of this lane's row -> packed
+// fp16 pairs in A_h columns [c0/2, c0/2 + NC/2) (NC = HID / 2: each of the
+// two warps of a lane quadrant takes half of the columns). The bias is
+// already in D (constant-operand K-step / A_h bias column) and the
+// activation scale carries through the positively homogeneous leaky-ReLU.
+template <int NC>
+__device__ __forceinline__ void epi_hidden(uint32_t tD, uint32_t tA, int c0) {
+  static_assert(NC == 64 || NC == 32, "32 or 64 columns per warp");
   uint32_t a0[32], a1[32], o[32];
   tc::tmem_ld32(tD + c0, a0);
-  tc::tmem_ld32(tD + c0 + 32, a1);
+  if (NC == 64) tc::tmem_ld32(tD + c0 + 32, a1);
   tc::tmem_wait_ld();
 #pragma unroll
   for (int j = 0; j < 16; ++j) o[j] = leaky_pack(a0[2 * j], a0[2 * j + 1]);
+  if (NC == 64) {
 #pragma unroll
-  for (int j = 0; j < 16; ++j) o[16 + j] = leaky_pack(a1[2 * j], a1[2 * j + 1]);
-  tc::tmem_st32(tA + c0 / 2, o);
+    for (int j = 0; j < 16; ++j) o[16 + j] = leaky_pack(a1[2 * j], a1[2 * j + 1]);
+    tc::tmem_st32(tA + c0 / 2, o);
+  } else {
+    tc::tmem_st16(tA + c0 / 2, o);
+  }
 }
 
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
@@ -402,7 +409,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   constexpr int K2 = Lay::kK2;
   constexpr int EW = Lay::kEpiWarps;
   constexpr int NS = Lay::kXStages;
-  static_assert(HID == 128, "the TS-form MLP kernel is specialised for hidden width 128");
+  static_assert(HID == 128 || HID == 64, "hidden width 64 (low-quality LSNIF) or 128 (high-quality)");
   const DevModel& m = P.m;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t xbytes = static_cast<uint32_t>(kTileM) * m.K1P * 2;
@@ -666,7 +673,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
         tc::mbar_wait(l_done + g, lcount++ & 1);
         if (tl) TL_STAMP(i * 64 + 8 + 8 * layer + e);  // L1 / L2 done seen by warp e
         tc::tc_fence_after();
-        epi_hidden64(tD, tA, half * 64);
+        epi_hidden<HID / 2>(tD, tA, half * (HID / 2));
         tc::tmem_wait_st();
         tc::tc_fence_before();
         __syncwarp();
@@ -1049,25 +1056,23 @@ cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st) {
   return fast ? launch_trace_t<false, 2, 3, true, 32>(p, st) : launch_trace_t<false, 0, 0, false, 0>(p, st);
 }
 
-cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st) {
-  if (max_tiles <= 0) return cudaSuccess;
+template <int HID>
+static cudaError_t launch_mlp_t(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st) {
   const size_t smem = mlp_smem_bytes(p.m);
   const unsigned grid = static_cast<unsigned>(std::min(max_tiles, num_sms));
-  thread_local LaunchCfg cfg[2];
+  thread_local LaunchCfg c;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (p.m.hidden != 128) return cudaErrorNotSupported;
-  LaunchCfg& c = cfg[1];
   if (c.dev != dev || c.smem != smem) {
     cudaError_t e =
-        cudaFuncSetAttribute(mlp_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaFuncSetAttribute(mlp_tc_kernel<HID>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     c.dev = dev;
     c.smem = smem;
   }
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(grid);
-  lc.blockDim = dim3(MlpLayout<128>::kThreads);
+  lc.blockDim = dim3(MlpLayout<HID>::kThreads);
   lc.dynamicSmemBytes = smem;
   lc.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1075,7 +1080,14 @@ cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStrea
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  return cudaLaunchKernelEx(&lc, mlp_tc_kernel<128>, p);
+  return cudaLaunchKernelEx(&lc, mlp_tc_kernel<HID>, p);
+}
+
+cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st) {
+  if (max_tiles <= 0) return cudaSuccess;
+  if (p.m.hidden == 128) return launch_mlp_t<128>(p, max_tiles, num_sms, st);
+  if (p.m.hidden == 64) return launch_mlp_t<64>(p, max_tiles, num_sms, st);
+  return cudaErrorNotSupported;
 }
 
 cudaError_t launch_infer_f32(const DevModel& m, const float* x, int64_t n, const lsnif_interval* iv,

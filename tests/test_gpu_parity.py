@@ -163,3 +163,29 @@ def test_bad_mode_raises(gmodel):
     rays = lsnif.rays_to_tensor(W.camera_rays(8, 8))
     with pytest.raises(ValueError):
         gmodel.query(rays, mode=7)
+
+
+@pytest.mark.parametrize("hidden,n_mat", [(64, 2), (128, 5)])
+def test_query_parity_other_widths(gmodel, oracle_teapot, tmp_path, hidden, n_mat):
+    """The paper's low-quality LSNIF (hidden width 64) and a wider material
+    head: a random-init model (make_sparse_hash_grid + make_mlp, seed 4) on
+    the teapot's occupancy and frame, saved and loaded through the file
+    format, queried through the same gates."""
+    from oracle import oracle as O
+    om = O.OracleModel.random(oracle_teapot.occupancy(), oracle_teapot.V, oracle_teapot.H,
+                              oracle_teapot.level_res, oracle_teapot.F, oracle_teapot.M, hidden, n_mat,
+                              oracle_teapot.aabb, 4)
+    path = str(tmp_path / f"h{hidden}.lsnif")
+    om.save(path)
+    om = O.OracleModel.load(path)  # the binary16 values both sides use
+    gm = lsnif.GpuModel(path)
+    assert gm.info.hidden == hidden and gm.info.n_mat == n_mat
+    for name in ("c1_camera_256", "c3_incoherent_64k"):
+        rays = workload_sets(gm.aabb)[name]
+        ref = om.narrow_phase(rays, 0, 0)
+        got = lsnif.hits_to_numpy(gm.query(lsnif.rays_to_tensor(rays)))
+        tr = om.trace(rays)
+        span = tr["interval"][:, 1] - tr["interval"][:, 0]
+        vis, mat, both, dt = compare_query(got, ref, name)
+        assert vis >= 0.999 and mat >= 0.999, (hidden, name, vis, mat)
+        assert np.all(dt[both] <= 2e-3 * span[both] + 1e-6)
