@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "lsnif_device.cuh"
@@ -31,7 +32,10 @@ namespace lsnif_dev {
 // then a warp-cooperative encode of all pooled points. LS/FS: compile-time
 // level/feature counts (0 = read from the model); POW2: M is a power of two.
 template <bool DEBUG, int LS, int FS, bool POW2, int VS>
-__global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams P) {
+#ifndef LSNIF_TRACE_MIN_BLOCKS
+#define LSNIF_TRACE_MIN_BLOCKS 8
+#endif
+__global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kernel(const TraceParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   const DevModel& m = P.m;
   const int L = LS ? LS : m.L;
@@ -46,9 +50,17 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
   for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.stop + i);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  uint2* pool = reinterpret_cast<uint2*>(smem + ((occ_words + 3) & ~3)) + warp * (H * 32);
-  // per-lane local ray (o, d) + MLP row, read by the encoding lanes
-  float4* lane_ray = reinterpret_cast<float4*>(smem + ((occ_words + 3) & ~3) + 4 * 2 * H * 32) + warp * 64;
+  // point pool per warp: entry t (fp32) and code (axis | plane << 2) in
+  // separate arrays, H x 32 each (5 or 6 bytes per point)
+  using code_t = typename std::conditional<(VS != 0 && VS < 64), uint8_t, uint16_t>::type;
+  float4* lane_ray = reinterpret_cast<float4*>(smem + ((occ_words + 3) & ~3)) + warp * 64;
+  float* pool_t = reinterpret_cast<float*>(smem + ((occ_words + 3) & ~3) + 4 * 64 * 4) + warp * (H * 32);
+  code_t* pool_c = reinterpret_cast<code_t*>(pool_t - warp * (H * 32) + 4 * H * 32) + warp * (H * 32);
+  auto pool_put = [&](int i, uint2 e) {
+    pool_t[i] = __uint_as_float(e.x);
+    pool_c[i] = static_cast<code_t>(e.y);
+  };
+  auto pool_get = [&](int i) -> uint2 { return make_uint2(__float_as_uint(pool_t[i]), pool_c[i]); };
   __syncthreads();
   const float scale = m.act_scale;
   const int64_t nbatch = (P.n + 127) / 128;
@@ -95,7 +107,7 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
     if (pair && walk_setup<VS>(m, o, d, t_min, w)) {
       if (stop_bit(smem, w.idx)) {  // start cell (always inside the grid)
         fio = w.axis0 < 0;
-        pool[lane] = pack_point(w.t0, w.axis0, w.plane0);
+        pool_put(lane, pack_point(w.t0, w.axis0, w.plane0));
         if (DEBUG) {
           int c[3];
           walk_cell<VS>(m, w.idx, c);
@@ -119,7 +131,7 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
             const float da = p2 ? w.d[2] : (p1 ? w.d[1] : w.d[0]);
             const int plane = static_cast<int>(rintf(__fmul_rn(__fadd_rn(oa, __fmul_rn(tn, da)), m.fres)));
             if (plane == (da > 0.0f ? V : 0)) break;
-            pool[count * 32 + lane] = pack_point(tn, axis, static_cast<float>(plane));
+            pool_put(count * 32 + lane, pack_point(tn, axis, static_cast<float>(plane)));
             if (DEBUG) {
               int c[3];
               walk_cell<VS>(m, w.idx, c);
@@ -291,9 +303,9 @@ __global__ void __launch_bounds__(128, 8) trace_encode_kernel(const TraceParams 
       const float ro[3] = {rq.x, rq.y, rq.z}, rd[3] = {rr.x, rr.y, rr.z};
       const int k = o_vc + j - o_excl;
       encode_point(std::false_type{}, ro, rd, wbatch * 32 + owner, __float_as_int(rq.w), __float_as_int(rr.w), k,
-                   pool[k * 32 + owner]);
+                   pool_get(k * 32 + owner));
     }
-    if (vc) encode_point(std::true_type{}, w.o, w.d, ray_idx, row, bin, 0, pool[lane]);
+    if (vc) encode_point(std::true_type{}, w.o, w.d, ray_idx, row, bin, 0, pool_get(lane));
 
     // ---- zero padding of the row tail up to the bin width (encoding.hpp:170)
     if (!DEBUG && valid) {
@@ -1007,7 +1019,8 @@ cudaError_t compute_zero_hit(const DevModel& m, lsnif_hit* host_out) {
 
 size_t trace_smem_bytes(const DevModel& m) {
   const size_t occ_words = static_cast<size_t>(m.stop_words);
-  return ((occ_words + 3) & ~size_t(3)) * 4 + 4 * static_cast<size_t>(m.H) * 32 * 8 + 4 * 64 * 16;
+  const bool fast = m.L == 2 && m.F == 3 && m.M_pow2 && m.V == 32;  // 1-byte point codes
+  return ((occ_words + 3) & ~size_t(3)) * 4 + 4 * 64 * 16 + 4 * static_cast<size_t>(m.H) * 32 * (fast ? 5 : 6);
 }
 
 size_t mlp_smem_bytes(const DevModel& m) {
@@ -1036,8 +1049,13 @@ static cudaError_t launch_trace_t(const TraceParams& p, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
+    if (const char* c = std::getenv("LSNIF_TRACE_CARVEOUT")) {  // A/B probe: shared-memory share (%)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(c));
+      if (e != cudaSuccess) return e;
+    }
     cudaDeviceGetAttribute(&cfg.sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.per_sm, kern, 128, smem);
+    if (const char* c = std::getenv("LSNIF_TRACE_BLOCKS")) cfg.per_sm = std::min(cfg.per_sm, std::atoi(c));
     cfg.dev = dev;
     cfg.smem = smem;
   }

@@ -50,7 +50,8 @@ for lib in libs:
                      trace_ms=p["trace_ms"] / reps, mlp_ms=p["mlp_ms"] / reps)
             r["grays_s_trace"] = d.shape[0] / r["trace_ms"] / 1e6
             r["query_ms"] = tot / reps
-            r["sort"] = os.environ.get("LSNIF_TRACE_SORT", "1")
+            r["carve"] = os.environ.get("LSNIF_TRACE_CARVEOUT", "")
+            r["blocks"] = os.environ.get("LSNIF_TRACE_BLOCKS", "")
             r["stats"] = st
             res.append(r)
             print(json.dumps(r), flush=True)
