@@ -346,6 +346,21 @@ def run_c4(args, rank, world, dev, gpu, max_over_ranks):
     elapsed_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
     value = world * len(rays) * args.steps / (elapsed_ms / 1e3)
     hits = lsnif.scene_hits_to_numpy(out)
+
+    # ---- e2e: same step through lsnif_scene_query_host (pinned host buffers)
+    pin_r = torch.from_numpy(rays.view(np.float32).reshape(-1, 8).copy()).pin_memory()
+    pin_h = torch.empty((len(rays), 16), dtype=torch.int32).pin_memory()
+    scene.query_host(pin_r, lsnif.CLOSEST, out=pin_h)
+    e2e_steps = max(3, min(args.steps, 10))
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        scene.query_host(pin_r, lsnif.CLOSEST, out=pin_h)
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    assert np.array_equal(pin_h.numpy(), out.cpu().numpy()), "host/device scene results differ"
     if rank == 0:
         tr = sum(p["trace_ms"] for p in profs) / args.steps
         ml = sum(p["mlp_ms"] for p in profs) / args.steps
@@ -359,8 +374,37 @@ def run_c4(args, rank, world, dev, gpu, max_over_ranks):
                 "workload_stats": {"frac_hit": float(np.mean(hits["flags"] == 1))},
                 "kernels": {"trace_encode_kernel": {"ms_per_step": tr},
                             "mlp_tc_kernel": {"ms_per_step": ml}},
+                "e2e": {"value": world * len(rays) * e2e_steps / e2e_s, "unit": UNIT,
+                        "h2d_bytes_per_step": 32 * len(rays), "d2h_bytes_per_step": 64 * len(rays),
+                        "steps": e2e_steps,
+                        "api": "lsnif_scene_query_host (pinned host rays/scene hits, chunked H2D/query/D2H)"},
                 "gpu_launches": launches,
                 "clocks": clocks.summary()}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                O = cpu_oracle(True)
+                om = [O.OracleModel.load(os.path.join(gold, n + ".lsnif"), fast=True) for n in W.C4_MODELS]
+                om = [om[k] for k in W.C4_INSTANCES]
+                probe = rays[:: max(1, len(rays) // 8192)]
+                t0 = time.perf_counter()
+                O.scene_query(om, w2o, probe, 0, 0)
+                rate = len(probe) / max(time.perf_counter() - t0, 1e-6)
+                stride = max(1, int(len(rays) / max(rate * args.cpu_seconds, 1.0)))
+                sample = rays[::stride]
+                # whole frame shorter than the target: repeat it (best of nothing, total time)
+                reps = max(1, int(round(args.cpu_seconds * rate / len(sample))))
+                t0 = time.perf_counter()
+                for _ in range(reps):
+                    O.scene_query(om, w2o, sample, 0, 0)
+                dt = (time.perf_counter() - t0) / reps
+                line["cpu_baseline"] = {
+                    "value": len(sample) / dt, "unit": UNIT,
+                    "cores": int(O.lib(True).oracle_hardware_concurrency()), "kind": "port",
+                    "sample": f"every {stride}th C4 camera ray ({len(sample)} rays) x {reps} passes, oracle "
+                              f"scene_query (collect_pairs + per-object narrow phase + merge), "
+                              f"{reps * dt:.1f} s"}
+            except Exception as e:  # the baseline is reported, never the target
+                line["cpu_baseline"] = {"unavailable": str(e)[:200]}
         print(json.dumps(line), flush=True)
 
 

@@ -205,6 +205,12 @@ lsnif_status lsnif_scene_destroy(lsnif_scene scene);
  * WORLD-space DEVICE rays in, one lsnif_scene_hit per ray out. */
 lsnif_status lsnif_scene_query(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n, int mode,
                                lsnif_scene_hit* d_hits, void* stream);
+/* The same from HOST rays / results (intersect_scene's std::vector<Ray> in,
+ * one result per ray out): chunked H2D -> scene query -> D2H through
+ * per-scene staging buffers, ordered after `stream`; returns when h_hits is
+ * filled. Pinned host memory gets the full PCIe rate. */
+lsnif_status lsnif_scene_query_host(lsnif_scene scene, const lsnif_ray* h_rays, int64_t n, int mode,
+                                    lsnif_scene_hit* h_hits, void* stream);
 
 /* ---- wavefront path tracer ----
  * lsnif::Camera (scene.hpp:12-17), lsnif::Light (scene.hpp:19-26; point and

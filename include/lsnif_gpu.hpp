@@ -176,13 +176,9 @@ class Scene {
   // intersect_scene (renderer.cpp:269-303) / occluded_batch (305-323) for a
   // scene without triangle objects; WORLD-space host rays.
   std::vector<lsnif_scene_hit> query(const std::vector<lsnif_ray>& rays, int mode) const {
-    const size_t n = rays.size();
-    DeviceBuffer<lsnif_ray> dr(n);
-    DeviceBuffer<lsnif_scene_hit> dh(n);
-    std::vector<lsnif_scene_hit> out(n);
-    if (n) cudaMemcpy(dr.ptr, rays.data(), n * sizeof(lsnif_ray), cudaMemcpyHostToDevice);
-    check(lsnif_scene_query(h_.get(), dr.ptr, static_cast<int64_t>(n), mode, dh.ptr, nullptr));
-    if (n) cudaMemcpy(out.data(), dh.ptr, n * sizeof(lsnif_scene_hit), cudaMemcpyDeviceToHost);
+    std::vector<lsnif_scene_hit> out(rays.size());
+    check(lsnif_scene_query_host(h_.get(), rays.data(), static_cast<int64_t>(rays.size()), mode, out.data(),
+                                 nullptr));
     return out;
   }
   std::vector<std::optional<lsnif_scene_hit>> intersect_scene(const std::vector<lsnif_ray>& rays) const {

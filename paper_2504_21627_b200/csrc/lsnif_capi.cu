@@ -119,12 +119,13 @@ struct Workspace {
 // stream, so the H2D copy engine, the kernels and the D2H copy engine work on
 // different chunks at once (PCIe-bound; copies of a slot are stream-ordered).
 constexpr int kSlots = 4;
-struct HostStaging {
+template <typename Hit>
+struct HostStagingT {
   cudaStream_t streams[kSlots] = {};
   lsnif_ray* d_rays[kSlots] = {};
-  lsnif_hit* d_hits[kSlots] = {};
+  Hit* d_hits[kSlots] = {};
   int64_t cap = 0;
-  ~HostStaging() {
+  ~HostStagingT() {
     for (int i = 0; i < kSlots; ++i) {
       cudaFree(d_rays[i]);
       cudaFree(d_hits[i]);
@@ -132,15 +133,62 @@ struct HostStaging {
     }
   }
 };
+using HostStaging = HostStagingT<lsnif_hit>;
 
 constexpr int64_t kChunk = int64_t(1) << 21;      // rays per trace/MLP launch pair
 constexpr int64_t kHostChunk = int64_t(1) << 17;  // rays per host staging step (LSNIF_HOST_CHUNK overrides)
 
-int64_t host_chunk() {
+int64_t host_chunk(int64_t dflt = kHostChunk) {
   const char* e = std::getenv("LSNIF_HOST_CHUNK");
   const long long v = e ? std::atoll(e) : 0;
-  return v >= 1024 ? static_cast<int64_t>(v) : kHostChunk;
+  return v >= 1024 ? static_cast<int64_t>(v) : dflt;
 }
+// Chunked host round trip through kSlots staging slots: per chunk H2D of
+// the rays, query(d_rays, n, d_hits, stream), D2H of the results, each slot
+// on its own stream so the copy engines and the kernels overlap. The slots
+// are ordered after prior work on the caller's stream; returns when the
+// results are in host memory.
+// `chunk` = rays per staging step (LSNIF_HOST_CHUNK overrides).
+template <typename Hit, typename Query>
+void host_round_trip(std::unique_ptr<HostStagingT<Hit>>& staging, int64_t chunk, const lsnif_ray* h_rays,
+                     int64_t n, Hit* h_hits, cudaStream_t stream, Query&& query) {
+  if (!staging) {
+    auto s = std::make_unique<HostStagingT<Hit>>();
+    const int64_t cap = host_chunk(chunk);
+    for (int i = 0; i < kSlots; ++i) {
+      ck(cudaStreamCreateWithFlags(&s->streams[i], cudaStreamNonBlocking), "cudaStreamCreate");
+      ck(cudaMalloc(&s->d_rays[i], cap * sizeof(lsnif_ray)), "cudaMalloc(staging)");
+      ck(cudaMalloc(&s->d_hits[i], cap * sizeof(Hit)), "cudaMalloc(staging)");
+    }
+    s->cap = cap;
+    staging = std::move(s);
+  }
+  HostStagingT<Hit>& S = *staging;
+  cudaEvent_t ev;
+  ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+  struct EventGuard {
+    cudaEvent_t e;
+    ~EventGuard() { cudaEventDestroy(e); }
+  } guard{ev};
+  ck(cudaEventRecord(ev, stream), "cudaEventRecord");
+  for (int i = 0; i < kSlots; ++i) ck(cudaStreamWaitEvent(S.streams[i], ev, 0), "cudaStreamWaitEvent");
+  // At least ~8 chunks per call so the H2D of one chunk, the kernels of the
+  // previous and the D2H of the one before overlap even for small batches.
+  const int64_t step = std::min(S.cap, std::max<int64_t>(16384, ((n + 7) / 8 + 1023) / 1024 * 1024));
+  int64_t k = 0;
+  for (int64_t s = 0; s < n; s += step, ++k) {
+    const int slot = static_cast<int>(k % kSlots);
+    const int64_t cn = std::min(step, n - s);
+    cudaStream_t st = S.streams[slot];
+    ck(cudaMemcpyAsync(S.d_rays[slot], h_rays + s, cn * sizeof(lsnif_ray), cudaMemcpyHostToDevice, st),
+       "cudaMemcpyAsync(H2D)");
+    query(S.d_rays[slot], cn, S.d_hits[slot], st);
+    ck(cudaMemcpyAsync(h_hits + s, S.d_hits[slot], cn * sizeof(Hit), cudaMemcpyDeviceToHost, st),
+       "cudaMemcpyAsync(D2H)");
+  }
+  for (int i = 0; i < kSlots; ++i) ck(cudaStreamSynchronize(S.streams[i]), "cudaStreamSynchronize");
+}
+
 constexpr size_t kMaxChunks = 1024;                // chunks per query (2^31 rays / kChunk)
 // Counter block, zeroed by one memset per query (only the chunks it uses):
 // 4 x u64 stats, then per chunk {u64 batch counter, i32 row counter per K bin}.
@@ -655,8 +703,13 @@ struct lsnif_scene_s {
   std::map<cudaStream_t, std::unique_ptr<Scratch>> scratch;
   std::mutex render_mu;
   std::map<cudaStream_t, lsnif_pt::WorkspacePtr> render_ws;  // renderer path state per stream
+  std::mutex staging_mu;
+  std::unique_ptr<HostStagingT<lsnif_scene_hit>> staging;     // lsnif_scene_query_host
 
   ~lsnif_scene_s() {
+    cudaSetDevice(device);
+    staging.reset();
+    scratch.clear();
     cudaFree(boxes);
     for (cudaStream_t x : side) cudaStreamDestroy(x);
     for (cudaEvent_t e : side_done) cudaEventDestroy(e);
@@ -785,6 +838,25 @@ lsnif_status lsnif_scene_query(lsnif_scene scene, const lsnif_ray* d_rays, int64
                                lsnif_scene_hit* d_hits, void* stream) {
   return guarded([&] {
     lsnif_api::scene_query_async(scene, d_rays, n, nullptr, mode, d_hits, static_cast<cudaStream_t>(stream));
+  });
+}
+
+lsnif_status lsnif_scene_query_host(lsnif_scene scene, const lsnif_ray* h_rays, int64_t n, int mode,
+                                    lsnif_scene_hit* h_hits, void* stream) {
+  return guarded([&] {
+    if (!scene) fail(LSNIF_INVALID_ARGUMENT, "null scene");
+    if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
+    if (mode != LSNIF_QUERY_CLOSEST && mode != LSNIF_QUERY_ANY) fail(LSNIF_INVALID_ARGUMENT, "bad query mode");
+    if (n > 0 && (!h_rays || !h_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
+    if (n == 0) return;
+    ck(cudaSetDevice(scene->device), "cudaSetDevice");
+    std::lock_guard<std::mutex> lock(scene->staging_mu);
+    // larger steps than the single-model path: a scene chunk is ~4 launches
+    // per instance (scripts/scene_e2e_probe.py: C4 2^17 3.77 ms, 2^18 3.13 ms)
+    host_round_trip(scene->staging, 2 * kHostChunk, h_rays, n, h_hits, static_cast<cudaStream_t>(stream),
+                    [&](const lsnif_ray* r, int64_t cn, lsnif_scene_hit* h, cudaStream_t st) {
+                      lsnif_api::scene_query_async(scene, r, cn, nullptr, mode, h, st);
+                    });
   });
 }
 
@@ -940,39 +1012,10 @@ lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_
     if (n > 0 && (!h_rays || !h_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
     ck(cudaSetDevice(model->device), "cudaSetDevice");
     std::lock_guard<std::mutex> lock(model->staging_mu);
-    if (!model->staging) {
-      auto s = std::make_unique<HostStaging>();
-      const int64_t cap = host_chunk();
-      for (int i = 0; i < kSlots; ++i) {
-        ck(cudaStreamCreateWithFlags(&s->streams[i], cudaStreamNonBlocking), "cudaStreamCreate");
-        ck(cudaMalloc(&s->d_rays[i], cap * sizeof(lsnif_ray)), "cudaMalloc(staging)");
-        ck(cudaMalloc(&s->d_hits[i], cap * sizeof(lsnif_hit)), "cudaMalloc(staging)");
-      }
-      s->cap = cap;
-      model->staging = std::move(s);
-    }
-    HostStaging& S = *model->staging;
-    // Order the staging streams after prior work on the caller's stream.
-    cudaEvent_t ev;
-    ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
-    ck(cudaEventRecord(ev, static_cast<cudaStream_t>(stream)), "cudaEventRecord");
-    for (int i = 0; i < kSlots; ++i) ck(cudaStreamWaitEvent(S.streams[i], ev, 0), "cudaStreamWaitEvent");
-    // At least ~8 chunks per call so the H2D of one chunk, the kernels of the
-    // previous and the D2H of the one before overlap even for small batches.
-    const int64_t step = std::min(S.cap, std::max<int64_t>(16384, ((n + 7) / 8 + 1023) / 1024 * 1024));
-    int64_t k = 0;
-    for (int64_t s = 0; s < n; s += step, ++k) {
-      const int slot = static_cast<int>(k % kSlots);
-      const int64_t cn = std::min(step, n - s);
-      cudaStream_t st = S.streams[slot];
-      ck(cudaMemcpyAsync(S.d_rays[slot], h_rays + s, cn * sizeof(lsnif_ray), cudaMemcpyHostToDevice, st),
-         "cudaMemcpyAsync(H2D)");
-      run_query(*model, S.d_rays[slot], cn, mode, S.d_hits[slot], st);
-      ck(cudaMemcpyAsync(h_hits + s, S.d_hits[slot], cn * sizeof(lsnif_hit), cudaMemcpyDeviceToHost, st),
-         "cudaMemcpyAsync(D2H)");
-    }
-    for (int i = 0; i < kSlots; ++i) ck(cudaStreamSynchronize(S.streams[i]), "cudaStreamSynchronize");
-    cudaEventDestroy(ev);
+    host_round_trip(model->staging, kHostChunk, h_rays, n, h_hits, static_cast<cudaStream_t>(stream),
+                    [&](const lsnif_ray* r, int64_t cn, lsnif_hit* h, cudaStream_t st) {
+                      run_query(*model, r, cn, mode, h, st);
+                    });
   });
 }
 

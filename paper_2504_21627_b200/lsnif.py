@@ -84,6 +84,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.lsnif_scene_create.argtypes = [P, C.c_int32, C.POINTER(P)]
     lib.lsnif_scene_destroy.argtypes = [P]
     lib.lsnif_scene_query.argtypes = [P, P, C.c_int64, C.c_int, P, P]
+    lib.lsnif_scene_query_host.argtypes = [P, P, C.c_int64, C.c_int, P, P]
     lib.lsnif_profile_read.argtypes = [P, P, C.c_int, C.POINTER(Profile)]
     lib.lsnif_render.argtypes = [P, P, C.c_int32, P, P, C.c_int32, P, P, P, P, P]
     lib.lsnif_render_debug_paths.argtypes = [P, P, C.c_int64, C.c_int64, P, P, C.c_int32, P]
@@ -96,7 +97,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     for name in ("lsnif_model_load", "lsnif_model_destroy", "lsnif_model_get_info", "lsnif_query",
                  "lsnif_query_host", "lsnif_infer_batch", "lsnif_debug_traverse",
                  "lsnif_last_query_stats", "lsnif_profile_enable", "lsnif_profile_read",
-                 "lsnif_scene_create", "lsnif_scene_destroy", "lsnif_scene_query", "lsnif_render",
+                 "lsnif_scene_create", "lsnif_scene_destroy", "lsnif_scene_query",
+                 "lsnif_scene_query_host", "lsnif_render",
                  "lsnif_render_debug_paths", "lsnif_trainer_create_from_file", "lsnif_trainer_destroy",
                  "lsnif_trainer_step", "lsnif_trainer_export", "lsnif_trainer_batch_grad",
                  "lsnif_trainer_sample"):
@@ -313,6 +315,23 @@ class GpuScene:
             out = torch.empty((n, 16), dtype=torch.int32, device=rays.device)
         _check(load_library().lsnif_scene_query(self.h, rays.data_ptr(), n, mode, out.data_ptr(),
                                                 _stream_ptr(stream)))
+        return out
+
+    def query_host(self, rays: np.ndarray, mode: int = CLOSEST, out: np.ndarray | None = None):
+        """World-space HOST rays -> SCENE_HIT_DTYPE records (lsnif_scene_query_host:
+        chunked H2D / scene query / D2H). Pinned arrays get the full PCIe rate;
+        `rays` may be a RAY_DTYPE array or an (n, 8) float32 array/CPU tensor."""
+        if hasattr(rays, "data_ptr"):
+            n, src = rays.shape[0], rays.data_ptr()
+        else:
+            rays = np.ascontiguousarray(rays)
+            if rays.dtype != RAY_DTYPE:
+                rays = rays.astype(np.float32, copy=False).reshape(-1, 8)
+            n, src = len(rays), rays.ctypes.data
+        if out is None:
+            out = np.empty(n, SCENE_HIT_DTYPE)
+        dst = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        _check(load_library().lsnif_scene_query_host(self.h, src, n, mode, dst, None))
         return out
 
     def render(self, camera: dict, lights, environment, cfg: dict, world_diag, stream=None,

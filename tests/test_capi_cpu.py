@@ -94,6 +94,8 @@ def test_render_and_trainer_fail_loudly_without_gpu_work(tmp_path):
     assert lib.lsnif_render(None, None, 0, ctypes.byref(cam), None, 0, None, ctypes.byref(cfg), None, None,
                             None) == lsnif.INVALID_ARGUMENT
     assert b"null scene" in lib.lsnif_last_error()
+    assert lib.lsnif_scene_query_host(None, None, 4, 0, None, None) == lsnif.INVALID_ARGUMENT
+    assert b"null scene" in lib.lsnif_last_error()
     bad = lsnif._config(dict(width=0, height=8, spp=1, max_bounces=1))
     assert lib.lsnif_render_debug_paths(ctypes.byref(cam), ctypes.byref(bad), 0, 4, None, None, 0,
                                         None) == lsnif.INVALID_ARGUMENT

@@ -73,3 +73,19 @@ def test_scene_single_instance_matches_query(scenes):
     assert np.array_equal(sh["flags"] == 1, acc)
     assert np.array_equal(sh["t"][acc], h["t_world"][acc])
     assert np.array_equal(sh["albedo"][acc], h["albedo"][acc])
+
+
+@pytest.mark.parametrize("n,mode", [(1, 0), (70001, 0), (300000, 1)])
+def test_scene_query_host_matches_device(scenes, n, mode):
+    """lsnif_scene_query_host (chunked H2D / scene query / D2H over the
+    staging slots) returns the device path's records bit for bit, for one
+    chunk and for several (ragged last chunk), pageable and pinned buffers."""
+    gs = scenes[0]
+    rays = W.incoherent_rays(n, W.c4_bounds(), seed=7 + n)
+    dev = gs.query(lsnif.rays_to_tensor(rays), mode).cpu().numpy()
+    got = gs.query_host(rays, mode)
+    assert np.array_equal(got.view(np.int32).reshape(-1, 16), dev)
+    pin = torch.from_numpy(rays.view(np.float32).reshape(-1, 8).copy()).pin_memory()
+    out = torch.empty((n, 16), dtype=torch.int32).pin_memory()
+    gs.query_host(pin, mode, out=out)
+    assert np.array_equal(out.numpy(), dev)
