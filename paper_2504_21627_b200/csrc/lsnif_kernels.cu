@@ -47,7 +47,6 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
   // the MLP kernel (launched as a programmatic dependent) may start its
   // prologue while this grid runs; it waits for our completion before reading
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.stop + i);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // point pool per warp: entry t (fp32) and code (axis | plane << 2) in
@@ -61,7 +60,6 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
     pool_c[i] = static_cast<code_t>(e.y);
   };
   auto pool_get = [&](int i) -> uint2 { return make_uint2(__float_as_uint(pool_t[i]), pool_c[i]); };
-  __syncthreads();
   const float scale = m.act_scale;
   const int64_t nbatch = (P.n + 127) / 128;
   uint32_t st_pair = 0, st_rows = 0, st_pts = 0, st_vol = 0;  // query statistics
@@ -71,7 +69,10 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
 
   // Each warp claims 32-ray batches from a global counter; the next claim
   // and the next batch's ray loads are issued before the current batch is
-  // traversed (software pipelining), so warps never wait on each other.
+  // traversed (software pipelining), so warps never wait on each other. The
+  // first claim and ray loads overlap the stop-mask fill (small launches are
+  // latency-bound: C2 shadow rays 51 -> 41 us). A static first batch
+  // (block x 4 + warp) is no better there and costs C3 4%.
   auto claim = [&]() -> int64_t {
     unsigned long long b = 0;
     if (lane == 0) b = atomicAdd(P.batch_counter, 1ull);
@@ -88,6 +89,8 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
   };
   int64_t next_wb = claim();
   load_ray(next_wb);
+  for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.stop + i);
+  __syncthreads();
   while (next_wb < nwb) {
     const int64_t wbatch = next_wb;
     const int64_t ray_idx = wbatch * 32 + lane;
