@@ -20,6 +20,13 @@ int main(int argc, char** argv) {
     for (const auto& h : hits) n += h.has_value();
     std::printf("%d of %zu rays accepted a neural hit\n", n, rays.size());
 
+    // run_narrow_phase over given pairs: every ray with its [t_enter, t_exit]
+    std::vector<lsnif_interval> pairs(rays.size(), lsnif_interval{3.0f, 6.0f});
+    const auto nh = lsnif::gpu::infer_pairs(model, rays, pairs);
+    int occ = 0;
+    for (const auto& h : nh) occ += h.occluded;
+    std::printf("infer_pairs: %d of %zu pairs occluded\n", occ, nh.size());
+
     // render() of a one-instance scene (PrimaryMode::lsnif), 64x36 x 2 spp
     const lsnif::gpu::Scene scene({model}, {{1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0}});
     const lsnif_camera cam{{0.25f, 1.6f, 4.5f}, {0.25f, 0.87f, 0.0f}, {0.0f, 1.0f, 0.0f}, 40.0f};

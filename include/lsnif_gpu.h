@@ -139,6 +139,21 @@ lsnif_status lsnif_model_get_info(lsnif_model model, lsnif_model_info* out);
 lsnif_status lsnif_query(lsnif_model model, const lsnif_ray* d_rays, int64_t n, int mode,
                          lsnif_hit* d_hits, void* stream);
 
+/* run_narrow_phase proper (renderer.cpp:232-265): every ray is a pair of
+ * this object whose interval [t_enter, t_exit] (RayLsnifPair, renderer.hpp:33-38,
+ * from collect_pairs' ray_aabb_intersect, renderer.cpp:165-172) is given in
+ * d_intervals[i] instead of being recomputed; it feeds the t_world decode
+ * and the accept rule exactly as the recomputed one does. DEVICE pointers. */
+lsnif_status lsnif_query_pairs(lsnif_model model, const lsnif_ray* d_rays, const lsnif_interval* d_intervals,
+                               int64_t n, int mode, lsnif_hit* d_hits, void* stream);
+/* The two accept rules as separate entry points; d_intervals may be NULL
+ * (intervals clipped in the kernel, as lsnif_query) or the pairs' intervals
+ * (as lsnif_query_pairs). */
+lsnif_status lsnif_query_closest(lsnif_model model, const lsnif_ray* d_rays, const lsnif_interval* d_intervals,
+                                 int64_t n, lsnif_hit* d_hits, void* stream);
+lsnif_status lsnif_query_any(lsnif_model model, const lsnif_ray* d_rays, const lsnif_interval* d_intervals,
+                             int64_t n, lsnif_hit* d_hits, void* stream);
+
 /* Same with HOST rays/hits (pinned or pageable): chunked H2D / query / D2H,
  * overlapped on internal streams. Synchronous. */
 lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_t n, int mode,

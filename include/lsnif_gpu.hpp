@@ -136,6 +136,31 @@ inline std::vector<lsnif_hit> query(const Model& model, const std::vector<lsnif_
   return hits;
 }
 
+// run_narrow_phase (renderer.cpp:232-265) for one object group: the pairs'
+// object-space rays and their [t_enter, t_exit] (RayLsnifPair); one NeuralHit
+// per pair, in pair order, for the caller's accept lambdas. `mode` picks the
+// kernel's own accept flag (LSNIF_HIT_ACCEPTED in the raw hits, see query()).
+inline std::vector<NeuralHit> infer_pairs(const Model& model, const std::vector<lsnif_ray>& rays,
+                                          const std::vector<lsnif_interval>& pairs,
+                                          int mode = LSNIF_QUERY_CLOSEST) {
+  if (rays.size() != pairs.size()) throw std::invalid_argument("infer_pairs: one interval per ray");
+  const size_t n = rays.size();
+  DeviceBuffer<lsnif_ray> dr(n);
+  DeviceBuffer<lsnif_interval> di(n);
+  DeviceBuffer<lsnif_hit> dh(n);
+  if (n) {
+    cudaMemcpy(dr.ptr, rays.data(), n * sizeof(lsnif_ray), cudaMemcpyHostToDevice);
+    cudaMemcpy(di.ptr, pairs.data(), n * sizeof(lsnif_interval), cudaMemcpyHostToDevice);
+  }
+  check(lsnif_query_pairs(model.handle(), dr.ptr, di.ptr, static_cast<int64_t>(n), mode, dh.ptr, nullptr));
+  std::vector<lsnif_hit> raw(n);
+  if (n) cudaMemcpy(raw.data(), dh.ptr, n * sizeof(lsnif_hit), cudaMemcpyDeviceToHost);
+  std::vector<NeuralHit> out;
+  out.reserve(n);
+  for (const lsnif_hit& h : raw) out.push_back(to_neural_hit(h));
+  return out;
+}
+
 // Closest-hit narrow phase of intersect_scene for one LSNIF object at identity
 // transform: the accepted neural hit per ray, if any.
 inline std::vector<std::optional<NeuralHit>> intersect(const Model& model, const std::vector<lsnif_ray>& rays) {

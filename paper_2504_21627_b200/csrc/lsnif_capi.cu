@@ -607,7 +607,7 @@ void create_into(const lsnif_model_desc& d, int device, lsnif_model* out) {
 
 // n is the ray count, or its upper bound when n_dev (device-side count) is set.
 void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, lsnif_hit* d_hits,
-               cudaStream_t st, const int32_t* n_dev = nullptr) {
+               cudaStream_t st, const int32_t* n_dev = nullptr, const lsnif_interval* d_intervals = nullptr) {
   if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
   if (mode != LSNIF_QUERY_CLOSEST && mode != LSNIF_QUERY_ANY) fail(LSNIF_INVALID_ARGUMENT, "bad query mode");
   if (n > 0 && (!d_rays || !d_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
@@ -624,6 +624,7 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     lsnif_dev::TraceParams tp{};
     tp.m = M.dm;
     tp.rays = d_rays + s;
+    tp.intervals = d_intervals ? d_intervals + s : nullptr;
     tp.n = cn;
     tp.n_dev = n_dev;
     tp.offset = s;
@@ -1001,6 +1002,33 @@ lsnif_status lsnif_query(lsnif_model model, const lsnif_ray* d_rays, int64_t n, 
   return guarded([&] {
     check_model(model);
     run_query(*model, d_rays, n, mode, d_hits, static_cast<cudaStream_t>(stream));
+  });
+}
+
+lsnif_status lsnif_query_pairs(lsnif_model model, const lsnif_ray* d_rays, const lsnif_interval* d_intervals,
+                               int64_t n, int mode, lsnif_hit* d_hits, void* stream) {
+  return guarded([&] {
+    check_model(model);
+    if (n > 0 && !d_intervals) fail(LSNIF_INVALID_ARGUMENT, "null interval pointer");
+    run_query(*model, d_rays, n, mode, d_hits, static_cast<cudaStream_t>(stream), nullptr, d_intervals);
+  });
+}
+
+lsnif_status lsnif_query_closest(lsnif_model model, const lsnif_ray* d_rays, const lsnif_interval* d_intervals,
+                                 int64_t n, lsnif_hit* d_hits, void* stream) {
+  return guarded([&] {
+    check_model(model);
+    run_query(*model, d_rays, n, LSNIF_QUERY_CLOSEST, d_hits, static_cast<cudaStream_t>(stream), nullptr,
+              d_intervals);
+  });
+}
+
+lsnif_status lsnif_query_any(lsnif_model model, const lsnif_ray* d_rays, const lsnif_interval* d_intervals,
+                             int64_t n, lsnif_hit* d_hits, void* stream) {
+  return guarded([&] {
+    check_model(model);
+    run_query(*model, d_rays, n, LSNIF_QUERY_ANY, d_hits, static_cast<cudaStream_t>(stream), nullptr,
+              d_intervals);
   });
 }
 

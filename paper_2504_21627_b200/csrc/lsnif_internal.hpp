@@ -29,6 +29,7 @@ namespace lsnif_dev {
 struct TraceParams {
   DevModel m;
   const lsnif_ray* rays;
+  const lsnif_interval* intervals;  // optional pair intervals (run_narrow_phase's t_enter/t_exit)
   int64_t n;                  // rays in this launch (upper bound when n_dev is set)
   const int32_t* n_dev;       // optional device-side ray count of the whole query
   int64_t offset;             // first ray of this launch within the query

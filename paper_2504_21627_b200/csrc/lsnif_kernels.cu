@@ -101,7 +101,17 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
     float o[3] = {ra.x, ra.y, ra.z}, d[3] = {ra.w, rb.x, rb.y};
     const float t_min = rb.z, t_max = rb.w;
     float enter = 0.0f, exit = 0.0f;
-    const bool pair = live && frame_interval(m, o, d, t_min, t_max, enter, exit);
+    bool pair;
+    if (P.intervals) {  // given pairs (run_narrow_phase, renderer.cpp:232-265): every ray is one
+      if (live) {
+        const float2 iv = __ldg(reinterpret_cast<const float2*>(P.intervals) + ray_idx);
+        enter = iv.x;
+        exit = iv.y;
+      }
+      pair = live;
+    } else {
+      pair = live && frame_interval(m, o, d, t_min, t_max, enter, exit);
+    }
 
     // ---- DDA (dda.cpp:88-116): occupied-cell entry points into the pool
     Walk w;

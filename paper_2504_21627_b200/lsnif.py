@@ -77,6 +77,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.lsnif_model_get_info.argtypes = [P, C.POINTER(ModelInfo)]
     lib.lsnif_query.argtypes = [P, P, C.c_int64, C.c_int, P, P]
     lib.lsnif_query_host.argtypes = [P, P, C.c_int64, C.c_int, P, P]
+    lib.lsnif_query_pairs.argtypes = [P, P, P, C.c_int64, C.c_int, P, P]
+    lib.lsnif_query_closest.argtypes = [P, P, P, C.c_int64, P, P]
+    lib.lsnif_query_any.argtypes = [P, P, P, C.c_int64, P, P]
     lib.lsnif_infer_batch.argtypes = [P, P, C.c_int64, C.c_int64, P, C.c_int64, P, P]
     lib.lsnif_debug_traverse.argtypes = [P, P, C.c_int64] + [P] * 7 + [P]
     lib.lsnif_last_query_stats.argtypes = [P, P, C.POINTER(QueryStats)]
@@ -95,7 +98,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.lsnif_trainer_batch_grad.argtypes = [P, P, P, C.c_int64, P, P, P, P]
     lib.lsnif_trainer_sample.argtypes = [P, C.c_int64, C.c_int64, P, P, P]
     for name in ("lsnif_model_load", "lsnif_model_destroy", "lsnif_model_get_info", "lsnif_query",
-                 "lsnif_query_host", "lsnif_infer_batch", "lsnif_debug_traverse",
+                 "lsnif_query_host", "lsnif_query_pairs", "lsnif_query_closest", "lsnif_query_any",
+                 "lsnif_infer_batch", "lsnif_debug_traverse",
                  "lsnif_last_query_stats", "lsnif_profile_enable", "lsnif_profile_read",
                  "lsnif_scene_create", "lsnif_scene_destroy", "lsnif_scene_query",
                  "lsnif_scene_query_host", "lsnif_render",
@@ -167,6 +171,21 @@ class GpuModel:
             out = torch.empty((n, 8), dtype=torch.int32, device=rays.device)
         _check(load_library().lsnif_query(self.h, rays.data_ptr(), n, mode, out.data_ptr(),
                                           _stream_ptr(stream)))
+        return out
+
+    def query_pairs(self, rays, intervals, mode: int = CLOSEST, out=None, stream=None):
+        """run_narrow_phase (renderer.cpp:232-265): every ray is a pair with the
+        given [t_enter, t_exit] (CUDA tensor (n, 2) float32) instead of the
+        in-kernel frame clip. Returns (n, 8) int32 lsnif_hit records."""
+        torch = _torch()
+        assert rays.is_cuda and rays.dtype == torch.float32 and rays.shape[-1] == 8
+        assert intervals.is_cuda and intervals.dtype == torch.float32 and tuple(intervals.shape) == (rays.shape[0], 2)
+        rays, intervals = rays.contiguous(), intervals.contiguous()
+        n = rays.shape[0]
+        if out is None:
+            out = torch.empty((n, 8), dtype=torch.int32, device=rays.device)
+        _check(load_library().lsnif_query_pairs(self.h, rays.data_ptr(), intervals.data_ptr(), n, mode,
+                                                out.data_ptr(), _stream_ptr(stream)))
         return out
 
     def last_stats(self, stream=None) -> dict:

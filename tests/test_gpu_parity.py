@@ -189,3 +189,37 @@ def test_query_parity_other_widths(gmodel, oracle_teapot, tmp_path, hidden, n_ma
         vis, mat, both, dt = compare_query(got, ref, name)
         assert vis >= 0.999 and mat >= 0.999, (hidden, name, vis, mat)
         assert np.all(dt[both] <= 2e-3 * span[both] + 1e-6)
+
+
+def test_query_pairs_given_intervals(gmodel, oracle_teapot):
+    """lsnif_query_pairs (run_narrow_phase over given RayLsnifPairs): with the
+    collect_pairs intervals (the oracle's, bit-exact with the kernel's own
+    clip) the results equal lsnif_query's bit for bit; a stretched interval
+    moves t_world = enter + sigmoid(z1) (exit - enter) accordingly; the
+    lsnif_query_closest / lsnif_query_any entry points match both forms."""
+    rays = W.camera_rays(256, 256)
+    tr = oracle_teapot.trace(rays)
+    pair = (tr["info"] >> 9) & 1 == 1
+    pr, iv = rays[pair], np.ascontiguousarray(tr["interval"][pair])
+    t_r, t_iv = lsnif.rays_to_tensor(pr), torch.from_numpy(iv).cuda()
+    lib = lsnif.load_library()
+    for mode in (lsnif.CLOSEST, lsnif.ANY):
+        ref = gmodel.query(t_r, mode).cpu().numpy()
+        got = gmodel.query_pairs(t_r, t_iv, mode).cpu().numpy()
+        assert np.array_equal(got, ref)
+        fn = lib.lsnif_query_closest if mode == lsnif.CLOSEST else lib.lsnif_query_any
+        for ivp in (None, t_iv.data_ptr()):
+            out = torch.empty_like(t_r, dtype=torch.int32)
+            lsnif._check(fn(gmodel.h, t_r.data_ptr(), ivp, len(pr), out.data_ptr(), None))
+            torch.cuda.synchronize()
+            assert np.array_equal(out.cpu().numpy(), ref)
+    wide = iv.copy()
+    wide[:, 1] = iv[:, 0] + 2.0 * (iv[:, 1] - iv[:, 0])
+    a = lsnif.hits_to_numpy(gmodel.query_pairs(t_r, t_iv))
+    b = lsnif.hits_to_numpy(gmodel.query_pairs(t_r, torch.from_numpy(wide).cuda()))
+    assert np.array_equal(a["flags_material"] & 3, b["flags_material"] & 3)  # same MLP answers
+    occ = (a["flags_material"] & 2) != 0
+    np.testing.assert_allclose(b["t_world"][occ] - iv[occ, 0], 2.0 * (a["t_world"][occ] - iv[occ, 0]),
+                               rtol=1e-4, atol=1e-5)
+    with pytest.raises(ValueError):  # null intervals: INVALID_ARGUMENT
+        lsnif._check(lib.lsnif_query_pairs(gmodel.h, t_r.data_ptr(), None, len(pr), 0, t_r.data_ptr(), None))
