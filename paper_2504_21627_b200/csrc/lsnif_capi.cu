@@ -172,9 +172,15 @@ void host_round_trip(std::unique_ptr<HostStagingT<Hit>>& staging, int64_t chunk,
   } guard{ev};
   ck(cudaEventRecord(ev, stream), "cudaEventRecord");
   for (int i = 0; i < kSlots; ++i) ck(cudaStreamWaitEvent(S.streams[i], ev, 0), "cudaStreamWaitEvent");
-  // At least ~8 chunks per call so the H2D of one chunk, the kernels of the
-  // previous and the D2H of the one before overlap even for small batches.
-  const int64_t step = std::min(S.cap, std::max<int64_t>(16384, ((n + 7) / 8 + 1023) / 1024 * 1024));
+  // ~8 chunks per call so the H2D of one chunk, the kernels of the previous
+  // and the D2H of the one before overlap, but no chunk below 64K rays: a
+  // query launch pair has ~40 us of fixed latency (C2 shadow call, 116k rays:
+  // 16K-ray chunks 0.27 ms, 64K 0.19 ms; scripts/e2e_min.sh).
+  static const int64_t min_step = [] {
+    const char* e = std::getenv("LSNIF_HOST_MIN_CHUNK");  // A/B probe
+    return e ? std::max<int64_t>(1024, std::atoll(e)) : int64_t(65536);
+  }();
+  const int64_t step = std::min(S.cap, std::max<int64_t>(min_step, ((n + 7) / 8 + 1023) / 1024 * 1024));
   int64_t k = 0;
   for (int64_t s = 0; s < n; s += step, ++k) {
     const int slot = static_cast<int>(k % kSlots);
