@@ -1,6 +1,7 @@
 """Small end-to-end exercise of every kernel family for compute-sanitizer:
-query (trace + MLP), debug traverse, infer_batch, scene query, render, and
-two training steps."""
+query (trace + MLP; in-kernel clip, given pair intervals, host staging),
+debug traverse, infer_batch, scene query (device and host), render, and two
+training steps."""
 import os
 import sys
 
@@ -18,6 +19,9 @@ rays = lsnif.rays_to_tensor(np.concatenate([W.camera_rays(64, 48), W.incoherent_
 gm.query(rays, lsnif.CLOSEST)
 gm.query(rays, lsnif.ANY)
 gm.debug_traverse(rays[:512])
+ivs = torch.rand((rays.shape[0], 2), device="cuda").sort(dim=1).values * 4  # given pair intervals
+gm.query_pairs(rays, ivs, lsnif.CLOSEST)
+gm.query_host(rays.cpu().numpy().view(lsnif.RAY_DTYPE).reshape(-1), lsnif.ANY)
 x = torch.zeros((64, gm.input_width), dtype=torch.float32, device="cuda")
 iv = torch.zeros((64, 2), dtype=torch.float32, device="cuda")
 gm.infer_batch(x, iv)
@@ -25,6 +29,7 @@ models = [lsnif.GpuModel(os.path.join(gold, n + ".lsnif")) for n in W.RENDER_MOD
 w2o = W.render_world_to_object()
 scene = lsnif.GpuScene([(models[i], w2o[i]) for i in range(len(models))])
 scene.query(lsnif.rays_to_tensor(W.camera_rays(32, 24, camera=W.RENDER_CAMERA), "cuda"))
+scene.query_host(W.camera_rays(40, 30, camera=W.RENDER_CAMERA), lsnif.ANY)
 img = scene.render(W.RENDER_CAMERA, W.RENDER_LIGHTS, W.RENDER_ENV, dict(width=24, height=16, spp=2, max_bounces=2),
                    W.world_diag_from_frames([m.aabb for m in models]))
 verts, faces = O.shape_mesh(0)
