@@ -436,6 +436,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   constexpr int NS = Lay::kXStages;
   static_assert(HID == 128 || HID == 64, "hidden width 64 (low-quality LSNIF) or 128 (high-quality)");
   const DevModel& m = P.m;
+  if (blockIdx.x == 0 && threadIdx.x == 0) TL_STAMP(1023 * 64 + 0);  // kernel entry
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t xbytes = static_cast<uint32_t>(kTileM) * m.K1P * 2;
   const uint32_t xstage = (xbytes + 1023) & ~1023u;
@@ -496,6 +497,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     tc::bulk_g2s(sW3, m.w_canon + m.w1_bytes + m.w2_bytes, m.w3_bytes, w_full);
   }
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the trace kernel's rows are complete
+  if (blockIdx.x == 0 && threadIdx.x == 0) TL_STAMP(1023 * 64 + 1);  // dependency resolved
 
   // tiles of all K bins, bin-major: global tile -> (bin b, tile t within b)
   const int nb = m.n_bins;
@@ -561,6 +563,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       tc::mbar_wait(w_full, 0);
+      if (blockIdx.x == 0) TL_STAMP(1023 * 64 + 2);  // weights in SMEM
       const uint32_t sW1_a = tc::smem_addr(sW1), sW2_a = tc::smem_addr(sW2), sW3_a = tc::smem_addr(sW3);
       const uint32_t sX_a = tc::smem_addr(sX), sC_a = tc::smem_addr(sC);
       constexpr uint32_t kIdescH = tc::idesc_f16_f32(kTileM, HID);
@@ -737,6 +740,7 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     decode_pending();
   }
   __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) TL_STAMP(1023 * 64 + 3);  // all tiles done
   if (warp == 1) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, 2 * Lay::kGroupCols);

@@ -17,15 +17,23 @@ from paper_2504_21627_b200 import lsnif, workloads as W  # noqa: E402
 gm = lsnif.GpuModel(os.path.join(ROOT, "tests", "golden", "teapot_seed0.lsnif"))
 which = sys.argv[1] if len(sys.argv) > 1 else "c3"
 rays = W.incoherent_rays(1 << 21, gm.aabb, seed=3) if which == "c3" else W.camera_rays(1920, 1080)
+mode = lsnif.CLOSEST
+if which == "shadow":
+    hits = lsnif.hits_to_numpy(gm.query(lsnif.rays_to_tensor(rays, "cuda")))
+    rays, mode = W.shadow_rays(rays, hits, gm.aabb)[0], lsnif.ANY
 d = lsnif.rays_to_tensor(rays, "cuda")
-gm.query(d)
-gm.query(d)
+gm.query(d, mode)
+gm.query(d, mode)
 torch.cuda.synchronize()
 lib = lsnif.load_library()
 buf = np.zeros(1 << 16, np.uint64)
 assert lib.lsnif_probe_mlp_timeline(C.c_void_p(buf.ctypes.data), len(buf)) == 0
 T = buf.reshape(-1, 64).astype(np.int64)
+E = T[1023, :4].copy()  # CTA 0: entry, dependency resolved, weights in SMEM, all tiles done
+T[1023] = 0
 n = int(np.max(np.nonzero(T[:, 0])[0])) + 1
+print("CTA 0: entry->griddep wait %d, wait->weights %d, weights->first L1 issue %d, first L1 -> all done %d "
+      "(%d tiles), total %d cycles" % (E[1] - E[0], E[2] - E[1], T[0, 0] - E[2], E[3] - T[0, 0], n, E[3] - E[0]))
 T = T[:n]
 sl = T[4:n - 4]
 def med(x):
