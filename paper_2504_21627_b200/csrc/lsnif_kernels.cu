@@ -352,8 +352,9 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
 // Warp-specialised persistent MLP over the compacted 128-row X tiles:
 //   warp 0  loader: bulk-copies X tiles into a kXStages SMEM ring and keeps
 //           kPrefetch tiles ahead in flight as L2 prefetches;
-//   warp 1  TMEM allocator + one MMA-issuing thread that polls both groups'
-//           barriers and issues whichever layer is ready;
+//   warp 1  TMEM allocator + the MMA-issuing thread of epilogue group 0;
+//           the last warp issues group 1's MMAs (each blocks on its own
+//           group's barriers; the tensor pipe interleaves the streams);
 //   warps 2-9 / 10-17  two epilogue groups of 8 warps (2 per TMEM lane
 //           quadrant, each taking half of the columns); group g owns TMEM
 //           columns [256g, 256g+256): the fp32 accumulator D (128 cols) and
@@ -366,7 +367,7 @@ template <int HID>
 struct MlpLayout {
   static constexpr int kK2 = HID + 16;        // hidden + bias block
   static constexpr int kEpiWarps = 8;         // per group
-  static constexpr int kThreads = 32 * (2 + 2 * kEpiWarps);
+  static constexpr int kThreads = 32 * (3 + 2 * kEpiWarps);  // loader, 2 issuers, epilogues
   static constexpr int kXStages = 4;
   static constexpr uint32_t kGroupCols = HID == 128 ? 256 : 128;  // TMEM columns per group (D + A_h)
   static constexpr uint32_t kACol = HID;      // A_h column offset within a group
@@ -401,18 +402,6 @@ __device__ __forceinline__ void epi_hidden(uint32_t tD, uint32_t tA, int c0) {
   } else {
     tc::tmem_st16(tA + c0 / 2, o);
   }
-}
-
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(done)
-      : "r"(tc::smem_addr(bar)), "r"(parity)
-      : "memory");
-  return done != 0;
 }
 
 // LSNIF_MLP_TIMELINE builds record, for CTA 0, clock64 stamps of the MMA
@@ -559,71 +548,66 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
         tc::bulk_g2s(sX + st * xstage, src, nbytes, x_full + st);
       }
     }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
+  } else if (warp == 1 || warp == 2 + 2 * EW) {
+    // ------------------------------------------------------------ MMA issuers
+    // one issuing thread per epilogue group (warp 1: group 0, the last warp:
+    // group 1), each blocking on its own group's barriers; the tensor pipe
+    // interleaves the two streams, so neither group's next layer waits for
+    // the other group's MMA burst to be issued
     if (lane == 0) {
+      const int g = warp == 1 ? 0 : 1;
       tc::mbar_wait(w_full, 0);
-      if (blockIdx.x == 0) TL_STAMP(1023 * 64 + 2);  // weights in SMEM
+      if (blockIdx.x == 0 && g == 0) TL_STAMP(1023 * 64 + 2);  // weights in SMEM
       const uint32_t sW1_a = tc::smem_addr(sW1), sW2_a = tc::smem_addr(sW2), sW3_a = tc::smem_addr(sW3);
       const uint32_t sX_a = tc::smem_addr(sX), sC_a = tc::smem_addr(sC);
       constexpr uint32_t kIdescH = tc::idesc_f16_f32(kTileM, HID);
       const uint32_t idesc3 = tc::idesc_f16_f32(kTileM, m.N3);
       constexpr uint32_t a_lbo = kTileM * 16;
-      int gi[2] = {0, 1}, gl[2] = {0, 0};
-      uint32_t hc[2] = {0, 0};
-      while (gi[0] < my_tiles || gi[1] < my_tiles) {
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          const int i = gi[g];
-          if (i >= my_tiles) continue;
-          const uint32_t tD = tmem + g * Lay::kGroupCols;
-          const uint32_t tA = tD + Lay::kACol;
-          if (gl[g] == 0) {
-            const int st = i % NS, kx = i / NS, ka = i >> 1;
-            if (!mbar_test(x_full + st, kx & 1)) continue;
-            if (ka > 0 && !mbar_test(acc_free + g, (ka - 1) & 1)) continue;
-            if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 5);  // X + accumulator ready seen
-            tc::tc_fence_after();
-            const uint32_t a_base = sX_a + st * xstage;
-            const int xb = x_bin[st];
-            for (int ks = 0; ks <= xb; ++ks) {  // L1: A = X (SMEM), the tile's bin width
-              // (the tile's SMEM stage holds K_b columns: LBO stays 128 x 16 B)
-              const uint64_t ad = tc::smem_desc(a_base + ks * 2 * a_lbo, a_lbo, 128);
-              const uint64_t bd = tc::smem_desc(sW1_a + ks * 2 * HID * 16, HID * 16, 128);
-              tc::mma_f16_ss(tD, ad, bd, kIdescH, ks > 0 ? 1u : 0u);
-            }
-            {  // + b1: constant slab (act_scale in column 0) x W1's bias slab
-              const uint64_t ad = tc::smem_desc(sC_a, a_lbo, 128);
-              const uint64_t bd = tc::smem_desc(sW1_a + (m.K1P / 16) * 2 * HID * 16, HID * 16, 128);
-              tc::mma_f16_ss(tD, ad, bd, kIdescH, 1u);
-            }
-            tc::mma_commit(x_empty + st);
-            if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 0);
-            gl[g] = 1;
-          } else {
-            if (!mbar_test(h_ready + g, hc[g] & 1)) continue;
-            if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 3 + (gl[g] - 1));  // h1 / h2 ready seen
-            ++hc[g];
-            tc::tc_fence_after();
-            if (gl[g] == 1) {  // L2: A = h1 (TMEM), K = HID + bias block
-              for (int ks = 0; ks < K2 / 16; ++ks) {
-                const uint64_t bd = tc::smem_desc(sW2_a + ks * 2 * HID * 16, HID * 16, 128);
-                tc::mma_f16_ts(tD, tA + ks * 8, bd, kIdescH, ks > 0 ? 1u : 0u);
-              }
-              gl[g] = 2;
-              if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 1);
-            } else {           // L3: A = h2 (TMEM), K = HID, N = 16
-              for (int ks = 0; ks < HID / 16; ++ks) {
-                const uint64_t bd = tc::smem_desc(sW3_a + ks * 2 * m.N3 * 16, m.N3 * 16, 128);
-                tc::mma_f16_ts(tD, tA + ks * 8, bd, idesc3, ks > 0 ? 1u : 0u);
-              }
-              gl[g] = 0;
-              if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 2);
-              gi[g] += 2;
-            }
-          }
-          tc::mma_commit(l_done + g);
+      const uint32_t tD = tmem + g * Lay::kGroupCols;
+      const uint32_t tA = tD + Lay::kACol;
+      uint32_t hc = 0;
+      for (int i = g; i < my_tiles; i += 2) {
+        const int st = i % NS, kx = i / NS, ka = i >> 1;
+        tc::mbar_wait(x_full + st, kx & 1);
+        if (ka > 0) tc::mbar_wait(acc_free + g, (ka - 1) & 1);
+        if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 5);  // X + accumulator ready seen
+        tc::tc_fence_after();
+        const uint32_t a_base = sX_a + st * xstage;
+        const int xb = x_bin[st];
+        for (int ks = 0; ks <= xb; ++ks) {  // L1: A = X (SMEM), the tile's bin width
+          // (the tile's SMEM stage holds K_b columns: LBO stays 128 x 16 B)
+          const uint64_t ad = tc::smem_desc(a_base + ks * 2 * a_lbo, a_lbo, 128);
+          const uint64_t bd = tc::smem_desc(sW1_a + ks * 2 * HID * 16, HID * 16, 128);
+          tc::mma_f16_ss(tD, ad, bd, kIdescH, ks > 0 ? 1u : 0u);
         }
+        {  // + b1: constant slab (act_scale in column 0) x W1's bias slab
+          const uint64_t ad = tc::smem_desc(sC_a, a_lbo, 128);
+          const uint64_t bd = tc::smem_desc(sW1_a + (m.K1P / 16) * 2 * HID * 16, HID * 16, 128);
+          tc::mma_f16_ss(tD, ad, bd, kIdescH, 1u);
+        }
+        tc::mma_commit(x_empty + st);
+        tc::mma_commit(l_done + g);
+        if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 0);
+        // L2: A = h1 (TMEM), K = HID + bias block
+        tc::mbar_wait(h_ready + g, hc++ & 1);
+        if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 3);  // h1 ready seen
+        tc::tc_fence_after();
+        for (int ks = 0; ks < K2 / 16; ++ks) {
+          const uint64_t bd = tc::smem_desc(sW2_a + ks * 2 * HID * 16, HID * 16, 128);
+          tc::mma_f16_ts(tD, tA + ks * 8, bd, kIdescH, ks > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(l_done + g);
+        if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 1);
+        // L3: A = h2 (TMEM), K = HID, N = 16
+        tc::mbar_wait(h_ready + g, hc++ & 1);
+        if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 4);  // h2 ready seen
+        tc::tc_fence_after();
+        for (int ks = 0; ks < HID / 16; ++ks) {
+          const uint64_t bd = tc::smem_desc(sW3_a + ks * 2 * m.N3 * 16, m.N3 * 16, 128);
+          tc::mma_f16_ts(tD, tA + ks * 8, bd, idesc3, ks > 0 ? 1u : 0u);
+        }
+        tc::mma_commit(l_done + g);
+        if (blockIdx.x == 0 && i < 1024) TL_STAMP(i * 64 + 2);
       }
     }
   } else {
