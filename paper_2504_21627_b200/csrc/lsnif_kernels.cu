@@ -488,10 +488,13 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the trace kernel's rows are complete
   if (blockIdx.x == 0 && threadIdx.x == 0) TL_STAMP(1023 * 64 + 1);  // dependency resolved
 
-  // tiles of all K bins, bin-major: global tile -> (bin b, tile t within b)
+  // tiles of all K bins, bin-major: global tile -> (bin b, tile t within b);
+  // one global round trip for the row counters (written by the trace grid)
   const int nb = m.n_bins;
+  if (tid < nb) bin_rows_n[tid] = P.row_counter[tid];
+  __syncthreads();
   int ntiles = 0;
-  for (int b = 0; b < nb; ++b) ntiles += (P.row_counter[b] + kTileM - 1) / kTileM;
+  for (int b = 0; b < nb; ++b) ntiles += (bin_rows_n[b] + kTileM - 1) / kTileM;
   if (static_cast<int>(blockIdx.x) >= ntiles) {  // nothing to do: release what the prologue took
     if (tid == 0) tc::mbar_wait(w_full, 0);
     __syncthreads();
@@ -505,10 +508,9 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     int acc = 0;
     for (int b = 0; b < nb; ++b) {
       tstart[b] = acc;
-      acc += (P.row_counter[b] + kTileM - 1) / kTileM;
+      acc += (bin_rows_n[b] + kTileM - 1) / kTileM;
     }
     tstart[nb] = acc;
-    for (int b = 0; b < nb; ++b) bin_rows_n[b] = P.row_counter[b];
   }
   __syncthreads();
   auto locate = [&](int tile, int& b, int& t) {
@@ -531,11 +533,19 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
         return P.X + bin_x_offset(b, P.cap_tiles) + static_cast<int64_t>(t) * bytes;
       };
       uint32_t nbytes;
-      for (int i = 0; i < kPrefetch && i < my_tiles; ++i) {
+      // the first stages' copies go out before any L2 prefetch (they would
+      // queue behind the prefetches in the copy engine)
+      for (int i = 0; i < NS && i < my_tiles; ++i) {
+        const uint8_t* src = tile_src(i, nbytes);
+        x_bin[i] = static_cast<int>(nbytes / kBinTileBytes) - 1;
+        tc::mbar_arrive_expect_tx(x_full + i, nbytes);
+        tc::bulk_g2s(sX + i * xstage, src, nbytes, x_full + i);
+      }
+      for (int i = NS; i < NS + kPrefetch && i < my_tiles; ++i) {
         const uint8_t* src = tile_src(i, nbytes);
         tc::bulk_prefetch_l2(src, nbytes);
       }
-      for (int i = 0; i < my_tiles; ++i) {
+      for (int i = NS; i < my_tiles; ++i) {
         const int st = i % NS, k = i / NS;
         if (i + kPrefetch < my_tiles) {
           const uint8_t* src = tile_src(i + kPrefetch, nbytes);
