@@ -373,11 +373,17 @@ struct MlpLayout {
   static constexpr uint32_t kACol = HID;      // A_h column offset within a group
 };
 
+// leaky_relu(v, 0.01) (mlp.hpp:80-94) as 0.505 v + 0.495 |v|: an FMUL and an
+// FFMA, both immediate forms on the FMA pipe, instead of FMUL + FMNMX (the
+// ALU pipe, which the epilogue saturates). The fp32 constants sum to exactly
+// 1 (slope 1 for v >= 0, within 1 ulp of v) and differ by 0.01 (1 - 9.5e-7)
+// for v < 0; the result is rounded to fp16 right after, so the difference to
+// fmaxf(v, 0.01 v) is below the fp16 rounding of the activations.
+__device__ __forceinline__ float leaky_fma(float v) {
+  return __fmaf_rn(fabsf(v), 0.495f, __fmul_rn(v, 0.505f));
+}
 __device__ __forceinline__ uint32_t leaky_pack(uint32_t a, uint32_t b) {
-  float v0 = __uint_as_float(a), v1 = __uint_as_float(b);
-  v0 = fmaxf(v0, __fmul_rn(v0, 0.01f));
-  v1 = fmaxf(v1, __fmul_rn(v1, 0.01f));
-  const __half2 h = __floats2half2_rn(v0, v1);
+  const __half2 h = __floats2half2_rn(leaky_fma(__uint_as_float(a)), leaky_fma(__uint_as_float(b)));
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
