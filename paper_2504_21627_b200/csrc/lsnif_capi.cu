@@ -698,12 +698,14 @@ struct lsnif_scene_s {
     int32_t* slots = nullptr;
     lsnif_hit* hits = nullptr;    // instance k's results at k * cap
     int32_t* count = nullptr;     // per instance
+    unsigned long long* best = nullptr;  // per ray: merge key (launch_merge_all)
     int64_t cap = 0;
     ~Scratch() {
       cudaFree(orays);
       cudaFree(slots);
       cudaFree(hits);
       cudaFree(count);
+      cudaFree(best);
     }
   };
   std::mutex mu;
@@ -735,12 +737,15 @@ struct lsnif_scene_s {
       cudaFree(s->orays);
       cudaFree(s->slots);
       cudaFree(s->hits);
+      cudaFree(s->best);
       s->orays = nullptr;
       s->slots = nullptr;
       s->hits = nullptr;
+      s->best = nullptr;
       ck(cudaMalloc(&s->orays, ni * n * sizeof(lsnif_ray)), "cudaMalloc(scene rays)");
       ck(cudaMalloc(&s->slots, ni * n * sizeof(int32_t)), "cudaMalloc(scene slots)");
       ck(cudaMalloc(&s->hits, ni * n * sizeof(lsnif_hit)), "cudaMalloc(scene hits)");
+      ck(cudaMalloc(&s->best, n * sizeof(unsigned long long)), "cudaMalloc(scene merge keys)");
       s->cap = n;
     }
     return *s;
@@ -766,8 +771,10 @@ void scene_query_async(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n, co
   }
   // one pass over the rays: scene hits initialised + every instance's pairs
   ck(cudaMemsetAsync(S.count, 0, ni * sizeof(int32_t), st), "cudaMemsetAsync");
+  // fused merge (two launches) unless pair indices overflow its 32-bit key
+  const bool fused = static_cast<uint64_t>(ni) * static_cast<uint64_t>(S.cap) < (uint64_t(1) << 32);
   ck(lsnif_dev::launch_broad_phase_all(scene->boxes, ni, d_rays, n, d_n, S.orays, S.slots, S.cap, S.count, d_hits,
-                                       st),
+                                       fused ? S.best : nullptr, st),
      "broad_phase_all_kernel");
   // narrow phases: independent per instance, concurrently on side streams
   constexpr int kMaxSide = 8;
@@ -791,10 +798,16 @@ void scene_query_async(lsnif_scene scene, const lsnif_ray* d_rays, int64_t n, co
     ck(cudaEventRecord(scene->side_done[q], scene->side[q]), "cudaEventRecord");
     ck(cudaStreamWaitEvent(st, scene->side_done[q], 0), "cudaStreamWaitEvent");
   }
-  for (int k = 0; k < ni; ++k)  // merges in object order (renderer.cpp:175-179)
-    ck(lsnif_dev::launch_merge(scene->models[k]->dm, scene->inst[k], d_rays, S.hits + k * S.cap,
-                               S.slots + k * S.cap, S.count + k, n, mode, d_hits, st),
-       "merge_kernel");
+  if (fused) {
+    ck(lsnif_dev::launch_merge_all(scene->boxes, ni, d_rays, n, d_n, S.hits, S.slots, S.cap, S.count, mode, S.best,
+                                   d_hits, st),
+       "merge_all");
+  } else {
+    for (int k = 0; k < ni; ++k)  // merges in object order (renderer.cpp:175-179)
+      ck(lsnif_dev::launch_merge(scene->models[k]->dm, scene->inst[k], d_rays, S.hits + k * S.cap,
+                                 S.slots + k * S.cap, S.count + k, n, mode, d_hits, st),
+         "merge_kernel");
+  }
 }
 
 }  // namespace lsnif_api
@@ -827,6 +840,8 @@ lsnif_status lsnif_scene_create(const lsnif_instance* instances, int32_t n, lsni
           boxes[k].mn[a] = instances[k].model->dm.mn[a];
           boxes[k].mx[a] = instances[k].model->dm.mx[a];
         }
+        boxes[k].materials = instances[k].model->dm.materials;
+        boxes[k].n_materials = instances[k].model->dm.n_materials;
       }
       ck(cudaSetDevice(S->device), "cudaSetDevice");
       ck(cudaMalloc(&S->boxes, boxes.size() * sizeof(lsnif_dev::InstanceBox)), "cudaMalloc(scene boxes)");

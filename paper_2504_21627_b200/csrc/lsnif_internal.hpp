@@ -71,14 +71,25 @@ struct InstanceParams {
 struct InstanceBox {
   float w2o[12];
   float mn[3], mx[3];  // the model's frame box
+  const lsnif_material* materials;  // the model's material table (DEVICE), for the merge
+  int32_t n_materials;
 };
 
 // collect_pairs for every instance in one pass over the rays (scene_init
 // fused): instance k's object-space rays / slots at orays / slots + k * stride,
 // its pair count at counts[k].
+// best (nullable): per-ray merge keys, reset to ~0 here for merge_all.
 cudaError_t launch_broad_phase_all(const InstanceBox* boxes, int n_inst, const lsnif_ray* rays, int64_t n,
                                    const int32_t* n_dev, lsnif_ray* orays, int32_t* slots, int64_t stride,
-                                   int32_t* counts, lsnif_scene_hit* out, cudaStream_t st);
+                                   int32_t* counts, lsnif_scene_hit* out, unsigned long long* best,
+                                   cudaStream_t st);
+// Accept + merge of every instance's neural hits in two launches (closest:
+// 64-bit atomicMin of (t, pair index) per ray, then the winner's SurfaceHit;
+// any: lowest occluding instance). Needs n_inst * stride < 2^32.
+cudaError_t launch_merge_all(const InstanceBox* boxes, int n_inst, const lsnif_ray* rays, int64_t n,
+                             const int32_t* n_dev, const lsnif_hit* hits, const int32_t* slots, int64_t stride,
+                             const int32_t* counts, int mode, unsigned long long* best, lsnif_scene_hit* out,
+                             cudaStream_t st);
 
 size_t trace_smem_bytes(const DevModel& m);
 cudaError_t compute_zero_hit(const DevModel& m, lsnif_hit* host_out);  // decode of z_zero, enter 0, exit 1

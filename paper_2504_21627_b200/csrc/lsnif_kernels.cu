@@ -820,7 +820,8 @@ __global__ void __launch_bounds__(256) broad_phase_all_kernel(const InstanceBox*
                                                               const lsnif_ray* __restrict__ rays, int64_t n,
                                                               const int32_t* n_dev, lsnif_ray* __restrict__ orays,
                                                               int32_t* __restrict__ slots, int64_t stride,
-                                                              int32_t* counts, lsnif_scene_hit* out) {
+                                                              int32_t* counts, lsnif_scene_hit* out,
+                                                              unsigned long long* best) {
   if (n_dev) n = min(n, static_cast<int64_t>(*n_dev));
   if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= n) return;  // whole block past the count
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -843,6 +844,7 @@ __global__ void __launch_bounds__(256) broad_phase_all_kernel(const InstanceBox*
     o[1] = make_float4(0.f, 0.f, 0.f, 0.f);
     o[2] = make_float4(0.f, 0.f, 0.f, 0.f);
     o[3] = make_float4(__int_as_float(-1), 0.f, 0.f, 0.f);
+    if (best) best[i] = ~0ull;
   }
   for (int k = 0; k < n_inst; ++k) {
     const InstanceBox& B = boxes[k];
@@ -890,10 +892,115 @@ __global__ void __launch_bounds__(256) broad_phase_all_kernel(const InstanceBox*
 
 cudaError_t launch_broad_phase_all(const InstanceBox* boxes, int n_inst, const lsnif_ray* rays, int64_t n,
                                    const int32_t* n_dev, lsnif_ray* orays, int32_t* slots, int64_t stride,
-                                   int32_t* counts, lsnif_scene_hit* out, cudaStream_t st) {
+                                   int32_t* counts, lsnif_scene_hit* out, unsigned long long* best,
+                                   cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   broad_phase_all_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(boxes, n_inst, rays, n, n_dev, orays,
-                                                                                slots, stride, counts, out);
+                                                                                slots, stride, counts, out, best);
+  return cudaGetLastError();
+}
+
+// Order-preserving map of a float onto uint32 (total order of non-NaN values).
+__device__ __forceinline__ uint32_t float_key(float t) {
+  const uint32_t b = __float_as_uint(t);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+// Pass 1 of the fused merge: every accepted neural hit of every instance
+// (grid.y = instance) offers its key. Closest (renderer.cpp:280-301): accept
+// iff occluded, t_min <= t < best_t with best_t starting at t_max; the object
+// loop keeps the smallest t and, among equal t, the first object, which is
+// the minimum of (t, k * stride + pair) since pairs of instance k sort before
+// those of k + 1. Any (316-321): occluded and t in [t_min, t_max]; the first
+// occluding object is the minimum k.
+__global__ void __launch_bounds__(256) merge_min_kernel(const lsnif_ray* __restrict__ rays,
+                                                        const lsnif_hit* __restrict__ hits,
+                                                        const int32_t* __restrict__ slots, int64_t stride,
+                                                        const int32_t* __restrict__ counts, int mode,
+                                                        unsigned long long* best) {
+  const int k = blockIdx.y;
+  const int64_t cnt = counts[k];
+  if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= cnt) return;
+  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j >= cnt) return;
+  const int64_t g = k * stride + j;
+  const uint32_t fm = hits[g].flags_material;
+  if (!(fm & LSNIF_HIT_OCCLUDED)) return;
+  const float t = hits[g].t_world;
+  const int32_t slot = slots[g];
+  const float t_min = rays[slot].t_min, t_max = rays[slot].t_max;
+  if (mode == LSNIF_QUERY_CLOSEST) {
+    if (!(t < t_max) || t < t_min) return;
+    atomicMin(best + slot, (static_cast<unsigned long long>(float_key(t)) << 32) | static_cast<uint32_t>(g));
+  } else if (t >= t_min && t <= t_max) {
+    atomicMin(best + slot, static_cast<unsigned long long>(k));
+  }
+}
+
+// Pass 2: the winner's SurfaceHit (as merge_kernel writes it) per ray.
+__global__ void __launch_bounds__(256) merge_final_kernel(const InstanceBox* __restrict__ boxes,
+                                                          const lsnif_ray* __restrict__ rays, int64_t n,
+                                                          const int32_t* n_dev, const lsnif_hit* __restrict__ hits,
+                                                          int64_t stride, int mode,
+                                                          const unsigned long long* __restrict__ best,
+                                                          lsnif_scene_hit* out) {
+  if (n_dev) n = min(n, static_cast<int64_t>(*n_dev));
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long key = best[i];
+  if (key == ~0ull) return;
+  if (mode != LSNIF_QUERY_CLOSEST) {
+    out[i].flags = 1u;
+    out[i].object_index = static_cast<int32_t>(key);
+    return;
+  }
+  const int64_t g = static_cast<int64_t>(key & 0xffffffffull);
+  const int k = static_cast<int>(g / stride);
+  const InstanceBox& B = boxes[k];
+  const lsnif_hit h = hits[g];
+  const lsnif_ray r = rays[i];
+  const float t = h.t_world;
+  lsnif_scene_hit o{};
+  o.t = t;
+  for (int a = 0; a < 3; ++a) o.position[a] = __fadd_rn(r.origin[a], __fmul_rn(t, r.direction[a]));
+  const float* n0 = h.normal;
+  float nw[3];
+  const float nn = __fadd_rn(__fadd_rn(__fmul_rn(n0[0], n0[0]), __fmul_rn(n0[1], n0[1])), __fmul_rn(n0[2], n0[2]));
+  if (nn == 0.0f) {
+    for (int a = 0; a < 3; ++a) nw[a] = -r.direction[a];
+  } else {  // normal_to_world (renderer.cpp:39-41): (W2O.linear^T n).normalized()
+    const float* L = B.w2o;
+    for (int a = 0; a < 3; ++a)
+      nw[a] = __fadd_rn(__fadd_rn(__fmul_rn(L[a], n0[0]), __fmul_rn(L[4 + a], n0[1])), __fmul_rn(L[8 + a], n0[2]));
+    const float len = sqrtf(__fadd_rn(__fadd_rn(__fmul_rn(nw[0], nw[0]), __fmul_rn(nw[1], nw[1])), __fmul_rn(nw[2], nw[2])));
+    if (len > 0.0f)
+      for (int a = 0; a < 3; ++a) nw[a] = __fdiv_rn(nw[a], len);
+  }
+  const float dd = __fadd_rn(__fadd_rn(__fmul_rn(nw[0], r.direction[0]), __fmul_rn(nw[1], r.direction[1])),
+                             __fmul_rn(nw[2], r.direction[2]));
+  for (int a = 0; a < 3; ++a) {
+    o.normal[a] = dd > 0.0f ? -nw[a] : nw[a];
+    o.albedo[a] = h.albedo[a];
+  }
+  const int mat = iclamp(static_cast<int>(h.flags_material >> LSNIF_HIT_MATERIAL_SHIFT), 0, B.n_materials - 1);
+  o.kind = B.materials[mat].kind;
+  o.roughness = B.materials[mat].roughness;
+  o.object_index = k;
+  o.flags = 1u;
+  out[i] = o;
+}
+
+cudaError_t launch_merge_all(const InstanceBox* boxes, int n_inst, const lsnif_ray* rays, int64_t n,
+                             const int32_t* n_dev, const lsnif_hit* hits, const int32_t* slots, int64_t stride,
+                             const int32_t* counts, int mode, unsigned long long* best, lsnif_scene_hit* out,
+                             cudaStream_t st) {
+  if (n <= 0 || n_inst <= 0) return cudaSuccess;
+  const dim3 g1(static_cast<unsigned>((stride + 255) / 256), static_cast<unsigned>(n_inst));
+  merge_min_kernel<<<g1, 256, 0, st>>>(rays, hits, slots, stride, counts, mode, best);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  merge_final_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(boxes, rays, n, n_dev, hits, stride,
+                                                                             mode, best, out);
   return cudaGetLastError();
 }
 
