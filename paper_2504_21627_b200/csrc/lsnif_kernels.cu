@@ -919,35 +919,29 @@ __global__ void __launch_bounds__(256) merge_min_kernel(const lsnif_ray* __restr
                                                         const int32_t* __restrict__ counts, int mode,
                                                         unsigned long long* best) {
   const int k = blockIdx.y;
-  const int64_t cnt = counts[k];
-  if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= cnt) return;
-  const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (j >= cnt) return;
-  const int64_t g = k * stride + j;
-  const uint32_t fm = hits[g].flags_material;
-  if (!(fm & LSNIF_HIT_OCCLUDED)) return;
-  const float t = hits[g].t_world;
-  const int32_t slot = slots[g];
-  const float t_min = rays[slot].t_min, t_max = rays[slot].t_max;
-  if (mode == LSNIF_QUERY_CLOSEST) {
-    if (!(t < t_max) || t < t_min) return;
-    atomicMin(best + slot, (static_cast<unsigned long long>(float_key(t)) << 32) | static_cast<uint32_t>(g));
-  } else if (t >= t_min && t <= t_max) {
-    atomicMin(best + slot, static_cast<unsigned long long>(k));
+  const int64_t cnt = counts[k];  // device-side pair count: grid-stride over it (the grid is sized by SMs)
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < cnt;
+       j += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = k * stride + j;
+    const uint32_t fm = hits[g].flags_material;
+    if (!(fm & LSNIF_HIT_OCCLUDED)) continue;
+    const float t = hits[g].t_world;
+    const int32_t slot = slots[g];
+    const float t_min = rays[slot].t_min, t_max = rays[slot].t_max;
+    if (mode == LSNIF_QUERY_CLOSEST) {
+      if (!(t < t_max) || t < t_min) continue;
+      atomicMin(best + slot, (static_cast<unsigned long long>(float_key(t)) << 32) | static_cast<uint32_t>(g));
+    } else if (t >= t_min && t <= t_max) {
+      atomicMin(best + slot, static_cast<unsigned long long>(k));
+    }
   }
 }
 
-// Pass 2: the winner's SurfaceHit (as merge_kernel writes it) per ray.
-__global__ void __launch_bounds__(256) merge_final_kernel(const InstanceBox* __restrict__ boxes,
-                                                          const lsnif_ray* __restrict__ rays, int64_t n,
-                                                          const int32_t* n_dev, const lsnif_hit* __restrict__ hits,
-                                                          int64_t stride, int mode,
-                                                          const unsigned long long* __restrict__ best,
-                                                          lsnif_scene_hit* out) {
-  if (n_dev) n = min(n, static_cast<int64_t>(*n_dev));
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const unsigned long long key = best[i];
+// The winner's SurfaceHit (as merge_kernel writes it) for ray i.
+__device__ __forceinline__ void merge_final_ray(const InstanceBox* __restrict__ boxes,
+                                                const lsnif_ray* __restrict__ rays, int64_t i,
+                                                const lsnif_hit* __restrict__ hits, int64_t stride, int mode,
+                                                unsigned long long key, lsnif_scene_hit* out) {
   if (key == ~0ull) return;
   if (mode != LSNIF_QUERY_CLOSEST) {
     out[i].flags = 1u;
@@ -990,17 +984,34 @@ __global__ void __launch_bounds__(256) merge_final_kernel(const InstanceBox* __r
   out[i] = o;
 }
 
+// Pass 2: the winners' SurfaceHits, grid-stride over the (device-side) ray count.
+__global__ void __launch_bounds__(256) merge_final_kernel(const InstanceBox* __restrict__ boxes,
+                                                          const lsnif_ray* __restrict__ rays, int64_t n,
+                                                          const int32_t* n_dev, const lsnif_hit* __restrict__ hits,
+                                                          int64_t stride, int mode,
+                                                          const unsigned long long* __restrict__ best,
+                                                          lsnif_scene_hit* out) {
+  if (n_dev) n = min(n, static_cast<int64_t>(*n_dev));
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    merge_final_ray(boxes, rays, i, hits, stride, mode, best[i], out);
+}
+
 cudaError_t launch_merge_all(const InstanceBox* boxes, int n_inst, const lsnif_ray* rays, int64_t n,
                              const int32_t* n_dev, const lsnif_hit* hits, const int32_t* slots, int64_t stride,
                              const int32_t* counts, int mode, unsigned long long* best, lsnif_scene_hit* out,
                              cudaStream_t st) {
   if (n <= 0 || n_inst <= 0) return cudaSuccess;
-  const dim3 g1(static_cast<unsigned>((stride + 255) / 256), static_cast<unsigned>(n_inst));
+  // grids sized for the machine, not for the upper-bound counts (the real
+  // counts live on the device; most of an n_max grid would exit at once)
+  constexpr int64_t kMaxBlocks = 148 * 8;
+  const dim3 g1(static_cast<unsigned>(std::min<int64_t>((stride + 255) / 256, std::max<int64_t>(kMaxBlocks / n_inst, 16))),
+                static_cast<unsigned>(n_inst));
   merge_min_kernel<<<g1, 256, 0, st>>>(rays, hits, slots, stride, counts, mode, best);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  merge_final_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(boxes, rays, n, n_dev, hits, stride,
-                                                                             mode, best, out);
+  merge_final_kernel<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, kMaxBlocks)), 256, 0, st>>>(
+      boxes, rays, n, n_dev, hits, stride, mode, best, out);
   return cudaGetLastError();
 }
 

@@ -25,6 +25,7 @@
 // normalisation as division by the square root), unfused.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -251,10 +252,8 @@ __global__ void __launch_bounds__(256) camera_kernel(const Params P, Paths S, in
 // with shade_hit, 378-442): miss -> environment; hit -> NEE shadow rays
 // (appended, contiguous per path), then the BSDF sample; continuing paths are
 // appended to the next bounce's list. The active count is read on the device.
-__global__ void __launch_bounds__(256) shade_kernel(const Params P, Paths S, int cur, int depth, int spawn) {
-  const int64_t n = S.counts[depth];
-  if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= n) return;  // whole block past the count
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void shade_one(const Params& P, Paths& S, int cur, int depth, int spawn, int64_t n,
+                                          int64_t k) {
   const int lane = threadIdx.x & 31;
   bool cont = false;
   lsnif_ray next{};
@@ -263,8 +262,8 @@ __global__ void __launch_bounds__(256) shade_kernel(const Params P, Paths S, int
   float scon[3 * kMaxShadows];
   int ns = 0;
   if (k < n) {
-    path = S.slots[cur][k];
-    const lsnif_ray ray = S.rays[cur][k];
+    path = (cur ? S.slots[1] : S.slots[0])[k];  // selects, not a dynamic index (keeps Paths out of local memory)
+    const lsnif_ray ray = (cur ? S.rays[1] : S.rays[0])[k];
     const lsnif_scene_hit h = S.hits[k];
     float thr[3];
 #pragma unroll
@@ -404,30 +403,39 @@ __global__ void __launch_bounds__(256) shade_kernel(const Params P, Paths S, int
   base = __shfl_sync(0xffffffffu, base, 0);
   if (cont) {
     const int j = base + __popc(m & ((1u << lane) - 1u));
-    S.rays[cur ^ 1][j] = next;
-    S.slots[cur ^ 1][j] = path;
+    (cur ? S.rays[0] : S.rays[1])[j] = next;
+    (cur ? S.slots[0] : S.slots[1])[j] = path;
   }
+}
+
+__global__ void __launch_bounds__(256) shade_kernel(const Params P, Paths S, int cur, int depth, int spawn) {
+  const int64_t n = S.counts[depth];
+  // block-stride over the device-side count (the grid is sized for the machine)
+  for (int64_t kb = static_cast<int64_t>(blockIdx.x) * blockDim.x; kb < n;
+       kb += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    shade_one(P, S, cur, depth, spawn, n, kb + threadIdx.x);
 }
 
 // occluded_batch result -> radiance (renderer.cpp:536-541), light order.
 __global__ void __launch_bounds__(256) shadow_accum_kernel(Paths S, int cur, int depth) {
   const int64_t n = S.counts[depth];
-  const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const int ns = S.shadow_n[k];
-  if (ns == 0) return;
-  const int first = S.shadow_first[k];
-  const int32_t path = S.slots[cur][k];
-  float rad[3];
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int ns = S.shadow_n[k];
+    if (ns == 0) continue;
+    const int first = S.shadow_first[k];
+    const int32_t path = (cur ? S.slots[1] : S.slots[0])[k];
+    float rad[3];
 #pragma unroll
-  for (int a = 0; a < 3; ++a) rad[a] = S.rad[3 * path + a];
-  for (int q = first; q < first + ns; ++q) {
-    if (S.shadow_hits[q].flags & 1u) continue;  // blocked
+    for (int a = 0; a < 3; ++a) rad[a] = S.rad[3 * path + a];
+    for (int q = first; q < first + ns; ++q) {
+      if (S.shadow_hits[q].flags & 1u) continue;  // blocked
 #pragma unroll
-    for (int a = 0; a < 3; ++a) rad[a] = __fadd_rn(rad[a], S.shadow_contrib[3 * q + a]);
+      for (int a = 0; a < 3; ++a) rad[a] = __fadd_rn(rad[a], S.shadow_contrib[3 * q + a]);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) S.rad[3 * path + a] = rad[a];
   }
-#pragma unroll
-  for (int a = 0; a < 3; ++a) S.rad[3 * path + a] = rad[a];
 }
 
 // Image accumulation (renderer.cpp:538-545): pixel += radiance of its
@@ -508,6 +516,15 @@ template <typename K, typename... A>
 void launch(K kern, int64_t n, cudaStream_t st, const char* what, A... args) {
   if (n <= 0) return;
   kern<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(args...);
+  ck(cudaGetLastError(), what);
+}
+
+// For kernels bounded by a device-side count (upper bound n): a grid sized
+// for the machine, the kernel strides over the real count.
+template <typename K, typename... A>
+void launch_strided(K kern, int64_t n, cudaStream_t st, const char* what, A... args) {
+  if (n <= 0) return;
+  kern<<<static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 148 * 8)), 256, 0, st>>>(args...);
   ck(cudaGetLastError(), what);
 }
 
@@ -623,11 +640,11 @@ void render(WorkspacePtr& wsp, lsnif_scene scene, const float* world_diag, int n
     for (int depth = 0; depth <= cfg.max_bounces; ++depth) {
       lsnif_api::scene_query_async(scene, S.rays[cur], n_paths, S.counts + depth, LSNIF_QUERY_CLOSEST, S.hits,
                                    st);
-      launch(shade_kernel, n_paths, st, "shade_kernel", P, S, cur, depth, depth < cfg.max_bounces ? 1 : 0);
+      launch_strided(shade_kernel, n_paths, st, "shade_kernel", P, S, cur, depth, depth < cfg.max_bounces ? 1 : 0);
       if (P.n_shadow_slots > 0) {
         lsnif_api::scene_query_async(scene, S.shadow_rays, n_paths * P.n_shadow_slots,
                                      S.counts + kMaxDepth + depth, LSNIF_QUERY_ANY, S.shadow_hits, st);
-        launch(shadow_accum_kernel, n_paths, st, "shadow_accum_kernel", S, cur, depth);
+        launch_strided(shadow_accum_kernel, n_paths, st, "shadow_accum_kernel", S, cur, depth);
       }
       cur ^= 1;
     }
