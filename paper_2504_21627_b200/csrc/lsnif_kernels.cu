@@ -816,15 +816,11 @@ __global__ void __launch_bounds__(256) broad_phase_kernel(const DevModel m, cons
 // ray is read once, its scene hit initialised (scene_init_kernel), and every
 // instance whose frame box it meets before t_max gets the object-space ray
 // appended to its own pair list (warp-aggregated per instance).
-__global__ void __launch_bounds__(256) broad_phase_all_kernel(const InstanceBox* __restrict__ boxes, int n_inst,
-                                                              const lsnif_ray* __restrict__ rays, int64_t n,
-                                                              const int32_t* n_dev, lsnif_ray* __restrict__ orays,
-                                                              int32_t* __restrict__ slots, int64_t stride,
-                                                              int32_t* counts, lsnif_scene_hit* out,
-                                                              unsigned long long* best) {
-  if (n_dev) n = min(n, static_cast<int64_t>(*n_dev));
-  if (static_cast<int64_t>(blockIdx.x) * blockDim.x >= n) return;  // whole block past the count
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void broad_phase_one(const InstanceBox* __restrict__ boxes, int n_inst,
+                                                const lsnif_ray* __restrict__ rays, int64_t n, int64_t i,
+                                                lsnif_ray* __restrict__ orays, int32_t* __restrict__ slots,
+                                                int64_t stride, int32_t* counts, lsnif_scene_hit* out,
+                                                unsigned long long* best) {
   const int lane = threadIdx.x & 31;
   const bool live = i < n;
   float p[3] = {0, 0, 0}, d[3] = {0, 0, 0}, t_min = 0.f, t_max = 0.f;
@@ -890,13 +886,27 @@ __global__ void __launch_bounds__(256) broad_phase_all_kernel(const InstanceBox*
   }
 }
 
+__global__ void __launch_bounds__(256) broad_phase_all_kernel(const InstanceBox* __restrict__ boxes, int n_inst,
+                                                              const lsnif_ray* __restrict__ rays, int64_t n,
+                                                              const int32_t* n_dev, lsnif_ray* __restrict__ orays,
+                                                              int32_t* __restrict__ slots, int64_t stride,
+                                                              int32_t* counts, lsnif_scene_hit* out,
+                                                              unsigned long long* best) {
+  if (n_dev) n = min(n, static_cast<int64_t>(*n_dev));
+  // block-stride over the (device-side) ray count: the grid is sized for the
+  // machine, every warp iterates uniformly (warp-aggregated appends)
+  for (int64_t kb = static_cast<int64_t>(blockIdx.x) * blockDim.x; kb < n;
+       kb += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    broad_phase_one(boxes, n_inst, rays, n, kb + threadIdx.x, orays, slots, stride, counts, out, best);
+}
+
 cudaError_t launch_broad_phase_all(const InstanceBox* boxes, int n_inst, const lsnif_ray* rays, int64_t n,
                                    const int32_t* n_dev, lsnif_ray* orays, int32_t* slots, int64_t stride,
                                    int32_t* counts, lsnif_scene_hit* out, unsigned long long* best,
                                    cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
-  broad_phase_all_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(boxes, n_inst, rays, n, n_dev, orays,
-                                                                                slots, stride, counts, out, best);
+  const unsigned grid = static_cast<unsigned>(n_dev ? std::min<int64_t>((n + 255) / 256, 148 * 8) : (n + 255) / 256);
+  broad_phase_all_kernel<<<grid, 256, 0, st>>>(boxes, n_inst, rays, n, n_dev, orays, slots, stride, counts, out, best);
   return cudaGetLastError();
 }
 
