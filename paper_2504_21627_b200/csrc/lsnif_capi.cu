@@ -663,6 +663,8 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     mp.cap_tiles = static_cast<int64_t>(w.x_tiles);
     mp.out = d_hits + s;
     mp.mode = mode;
+    mp.n_dev = n_dev;
+    mp.offset = s;
 
     if (M.profiling) {
       e0 = w.take_event();

@@ -59,6 +59,8 @@ struct MlpParams {
   int64_t cap_tiles;
   lsnif_hit* out;
   int mode;
+  const int32_t* n_dev;  // optional device-side ray count of the query (as TraceParams)
+  int64_t offset;        // first ray of this chunk within the query
 };
 
 // Multi-object scenes: one instance's placement.

@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
   // the MLP kernel (launched as a programmatic dependent) may start its
   // prologue while this grid runs; it waits for our completion before reading
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // a chunk past the device-side ray count: nothing to trace
+  if (P.n_dev && P.offset >= static_cast<int64_t>(*P.n_dev)) return;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   // point pool per warp: entry t (fp32) and code (axis | plane << 2) in
@@ -457,6 +459,10 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
+  // A chunk past the device-side ray count (renderer / scene queries sized by
+  // an upper bound) has no rows: leave before the prologue. The count was
+  // written before the trace kernel started, so it is visible here.
+  if (P.n_dev && P.offset >= static_cast<int64_t>(*P.n_dev)) return;
   // ---- prologue, independent of the trace kernel's results: with
   // programmatic dependent launch it overlaps the trace kernel's tail
   if (tid == 0) {
