@@ -75,11 +75,18 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
   // first claim and ray loads overlap the stop-mask fill (small launches are
   // latency-bound: C2 shadow rays 51 -> 41 us). A static first batch
   // (block x 4 + warp) is no better there and costs C3 4%.
-  auto claim = [&]() -> int64_t {
-    unsigned long long b = 0;
-    if (lane == 0) b = atomicAdd(P.batch_counter, 1ull);
-    return static_cast<int64_t>(__shfl_sync(0xffffffffu, b, 0));
+  // The claim is split: the atomic is issued at the top of a batch (the
+  // reservation point is unchanged, so batches stay balanced across warps)
+  // and its result is broadcast after the DDA, when the round trip of the
+  // contended same-address atomic is long complete (ncu: the broadcast right
+  // behind the atomic was the top stall, 13% of samples on C2); the next
+  // batch's rays then load during the encode.
+  unsigned int* const ctr = reinterpret_cast<unsigned int*>(P.batch_counter);
+  unsigned int pending = 0;
+  auto issue_claim = [&]() {
+    if (lane == 0) pending = atomicAdd(ctr, 1u);
   };
+  auto claimed = [&]() -> int64_t { return static_cast<int64_t>(__shfl_sync(0xffffffffu, pending, 0)); };
   float4 nra = make_float4(0, 0, 0, 0), nrb = nra;
   auto load_ray = [&](int64_t wb) {
     const int64_t r = wb * 32 + lane;
@@ -89,7 +96,8 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
       nrb = __ldg(r4 + 1);
     }
   };
-  int64_t next_wb = claim();
+  issue_claim();
+  int64_t next_wb = claimed();
   load_ray(next_wb);
   for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.stop + i);
   __syncthreads();
@@ -98,8 +106,7 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
     const int64_t ray_idx = wbatch * 32 + lane;
     const bool live = ray_idx < n_rays;
     const float4 ra = nra, rb = nrb;
-    next_wb = claim();
-    load_ray(next_wb);
+    issue_claim();
     float o[3] = {ra.x, ra.y, ra.z}, d[3] = {ra.w, rb.x, rb.y};
     const float t_min = rb.z, t_max = rb.w;
     float enter = 0.0f, exit = 0.0f;
@@ -157,6 +164,9 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
         }
       }
     }
+
+    next_wb = claimed();
+    load_ray(next_wb);
 
     // ---- rays answered without the MLP
     if (!DEBUG) {
