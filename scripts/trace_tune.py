@@ -21,7 +21,8 @@ for lib in libs:
     gm = lsnif.GpuModel(path, 0)
     prim = W.camera_rays(1920, 1080)
     hits = lsnif.hits_to_numpy(gm.query(lsnif.rays_to_tensor(prim, "cuda")))
-    sets = {"c2": lsnif.rays_to_tensor(prim, "cuda"),
+    sets = {"c1": lsnif.rays_to_tensor(W.camera_rays(256, 256), "cuda"),
+            "c2": lsnif.rays_to_tensor(prim, "cuda"),
             "c2shadow": lsnif.rays_to_tensor(W.shadow_rays(prim, hits, gm.aabb)[0], "cuda"),
             "c3": lsnif.rays_to_tensor(W.incoherent_rays(1 << 22, gm.aabb, seed=3), "cuda")}
     for dr in drains:
