@@ -223,3 +223,21 @@ def test_query_pairs_given_intervals(gmodel, oracle_teapot):
                                rtol=1e-4, atol=1e-5)
     with pytest.raises(ValueError):  # null intervals: INVALID_ARGUMENT
         lsnif._check(lib.lsnif_query_pairs(gmodel.h, t_r.data_ptr(), None, len(pr), 0, t_r.data_ptr(), None))
+
+
+def test_non_finite_rays_do_not_disturb_others(gmodel):
+    """NaN / Inf components (and zero directions) in some rays: the query
+    terminates, and every other ray's result is bit-identical to a batch
+    without them (no cross-ray contamination through shared tiles / rows)."""
+    good = W.incoherent_rays(20000, gmodel.aabb, seed=13)
+    bad = good[:512].copy()
+    k = np.arange(len(bad))
+    bad["d"][k % 4 == 0, 0] = np.nan
+    bad["o"][k % 4 == 1, 1] = np.inf
+    bad["d"][k % 4 == 2] = 0.0
+    bad["t_max"][k % 4 == 3] = np.nan
+    mixed = np.concatenate([good[:7000], bad, good[7000:]])
+    ref = gmodel.query(lsnif.rays_to_tensor(good)).cpu().numpy()
+    got = gmodel.query(lsnif.rays_to_tensor(mixed)).cpu().numpy()
+    torch.cuda.synchronize()
+    assert np.array_equal(np.concatenate([got[:7000], got[7000 + len(bad):]]), ref)
