@@ -213,6 +213,27 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU baseline
 
+def cpu_model() -> str:
+    """The host CPU's model name (the reference arm runs on these cores)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_detail(rate: float, cores: int, mlp_rows_per_ray: float, hidden: int, k1: int, n_out: int) -> dict:
+    """rays/s per core, the CPU model, and the CPU MLP GFLOP/s
+    (rows with >= 1 point x 2 (K1 H + H^2 + H n_out) FLOP) so the CPU GEMV is
+    visibly not a strawman."""
+    flop_row = 2 * (k1 * hidden + hidden * hidden + hidden * n_out)
+    return {"per_core": rate / max(cores, 1), "cpu_model": cpu_model(),
+            "mlp_gflops": rate * mlp_rows_per_ray * flop_row / 1e9}
+
+
 def cpu_oracle(fast: bool = True):
     from oracle import oracle as O
     if fast:
@@ -282,6 +303,12 @@ def run_reference(args, rank, world):
     n = len(prim) + len(shadow)
     total = sum(times)
     value = n * len(times) / total
+    # MLP rows per ray on a small subsample (oracle trace: rays with >= 1 point)
+    both = np.concatenate([prim, shadow]) if len(shadow) else prim
+    sub = both[:: max(1, len(both) // 8192)]
+    info = model.trace(sub)["info"]
+    rows = float(np.mean(((info >> 9) & 1 == 1) & ((info & 255) > 0)))
+    ref_detail = cpu_detail(value, cores, rows, model.hidden, model.input_width, 8 + model.n_mat)
     sample = (f"every {stride}th ray of the {args.workload.upper()} primary set "
               f"({len(prim)} rays) + {len(shadow)} shadow rays from the oracle's own hits")
     line = {
@@ -291,8 +318,8 @@ def run_reference(args, rank, world):
         "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload], "rays_per_step": n,
                    "parallelism": "host threads (parallel_slices)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": sample},
+        "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                              "sample": sample}, **ref_detail),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference cannot be built here (Eigen3/CLI11 absent); timed arm is the oracle's "
                 "C++ restatement of run_narrow_phase + infer_batch built with the reference's "
@@ -727,6 +754,8 @@ def main():
                     "sample": f"every {info['stride']}th primary and shadow ray of this "
                               f"workload ({info['rays']} rays), best of {info['reps']} passes "
                               f"(~{info['seconds']:.1f} s of CPU work)"}
+                line["cpu_baseline"].update(cpu_detail(rate, cores, rows / n_step, model.info.hidden,
+                                                       model.input_width, 8 + model.info.n_mat))
             except Exception as e:  # reported, never silently substituted
                 line["cpu_baseline"] = {"value": None, "error": str(e)}
         print(json.dumps(line), flush=True)
