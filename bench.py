@@ -213,6 +213,24 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU baseline
 
+def path_roofline(rays_per_s_gpu: float, n: int, rows: int, pts: int, vol: int, mlp_flops: float,
+                  peaks: dict) -> dict:
+    """SURVEY §8(d) whole-path ceiling per GPU: R_tensor = dense fp16 peak /
+    FLOP_ray, R_mem = HBM peak / B_ray (B_ray = 32 B ray + 32 B result + 48 B
+    per boundary point + 48 B per volume point), R_path = min of the two;
+    the path is issue/latency bound in traversal and encode, so this fraction
+    is small by construction (the per-kernel rooflines explain it)."""
+    flop_ray = mlp_flops / max(n, 1)
+    bytes_ray = 64.0 + 48.0 * (pts + vol) / max(n, 1)
+    tflops = peaks.get("bf16_tflops_sustained", 1400.0)
+    r_tensor = tflops * 1e12 / max(flop_ray, 1e-9)
+    r_mem = peaks["hbm_gbs"] * 1e9 / bytes_ray
+    r_path = min(r_tensor, r_mem)
+    return {"flop_per_ray": flop_ray, "bytes_per_ray": bytes_ray, "r_tensor": r_tensor, "r_mem": r_mem,
+            "r_path": r_path, "achieved": rays_per_s_gpu, "frac": rays_per_s_gpu / r_path,
+            "mlp_rows_per_ray": rows / max(n, 1), "unit": "rays/s per GPU"}
+
+
 def cpu_model() -> str:
     """The host CPU's model name (the reference arm runs on these cores)."""
     try:
@@ -729,6 +747,8 @@ def main():
                 "frac_ge1_point": rows / n_step, "mean_points": pts / n_step,
                 "volume_points": vol},
             "roofline": roof,
+            "path_roofline": path_roofline(value / world, n_step, rows, pts, vol,
+                                           mlp_flops, peaks),
             "kernels": {"trace_encode_kernel": {"ms_per_step": tr_ms,
                                                 "launches": prof["trace_launches"]},
                         "mlp_tc_kernel": {"ms_per_step": ml_ms,
