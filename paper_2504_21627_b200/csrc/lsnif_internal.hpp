@@ -93,7 +93,7 @@ cudaError_t launch_merge_all(const InstanceBox* boxes, int n_inst, const lsnif_r
                              const int32_t* counts, int mode, unsigned long long* best, lsnif_scene_hit* out,
                              cudaStream_t st);
 
-size_t trace_smem_bytes(const DevModel& m);
+size_t trace_smem_bytes(const DevModel& m, int warps_per_block);
 cudaError_t compute_zero_hit(const DevModel& m, lsnif_hit* host_out);  // decode of z_zero, enter 0, exit 1
 // n_dev (nullable): device-side ray count, n its upper bound
 cudaError_t launch_scene_init(const lsnif_ray* rays, int64_t n, const int32_t* n_dev, lsnif_scene_hit* out,

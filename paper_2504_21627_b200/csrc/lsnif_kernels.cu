@@ -31,11 +31,14 @@ namespace lsnif_dev {
 // 128-ray batches. Per warp: DDA per lane (points -> 8-byte pool entries),
 // then a warp-cooperative encode of all pooled points. LS/FS: compile-time
 // level/feature counts (0 = read from the model); POW2: M is a power of two.
-template <bool DEBUG, int LS, int FS, bool POW2, int VS>
-#ifndef LSNIF_TRACE_MIN_BLOCKS
-#define LSNIF_TRACE_MIN_BLOCKS 8
-#endif
-__global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kernel(const TraceParams P) {
+// TW: warps per block. Every block holds one SMEM copy of the stop mask, so
+// large blocks leave more of the unified L1 to the hash-table gathers and fill
+// fewer masks (TW = 32: one 1024-thread block per SM, for launches of many
+// waves); launches of about one wave use TW = 8, where 1024-thread blocks
+// would leave SMs idle (profiles/experiments: C2 primary TW 4/8/16/32 =
+// 0.144/0.140/0.138/0.135 ms, C2 shadow 0.041/0.039/0.043/0.048 ms).
+template <bool DEBUG, int LS, int FS, bool POW2, int VS, int TW>
+__global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const TraceParams P) {
   extern __shared__ __align__(16) uint32_t smem[];
   const DevModel& m = P.m;
   const int L = LS ? LS : m.L;
@@ -55,8 +58,8 @@ __global__ void __launch_bounds__(128, LSNIF_TRACE_MIN_BLOCKS) trace_encode_kern
   // separate arrays, H x 32 each (5 or 6 bytes per point)
   using code_t = typename std::conditional<(VS != 0 && VS < 64), uint8_t, uint16_t>::type;
   float4* lane_ray = reinterpret_cast<float4*>(smem + ((occ_words + 3) & ~3)) + warp * 64;
-  float* pool_t = reinterpret_cast<float*>(smem + ((occ_words + 3) & ~3) + 4 * 64 * 4) + warp * (H * 32);
-  code_t* pool_c = reinterpret_cast<code_t*>(pool_t - warp * (H * 32) + 4 * H * 32) + warp * (H * 32);
+  float* pool_t = reinterpret_cast<float*>(smem + ((occ_words + 3) & ~3) + TW * 64 * 4) + warp * (H * 32);
+  code_t* pool_c = reinterpret_cast<code_t*>(pool_t - warp * (H * 32) + TW * H * 32) + warp * (H * 32);
   auto pool_put = [&](int i, uint2 e) {
     pool_t[i] = __uint_as_float(e.x);
     pool_c[i] = static_cast<code_t>(e.y);
@@ -1178,10 +1181,11 @@ cudaError_t compute_zero_hit(const DevModel& m, lsnif_hit* host_out) {
   return e;
 }
 
-size_t trace_smem_bytes(const DevModel& m) {
+size_t trace_smem_bytes(const DevModel& m, int warps) {
   const size_t occ_words = static_cast<size_t>(m.stop_words);
   const bool fast = m.L == 2 && m.F == 3 && m.M_pow2 && m.V == 32;  // 1-byte point codes
-  return ((occ_words + 3) & ~size_t(3)) * 4 + 4 * 64 * 16 + 4 * static_cast<size_t>(m.H) * 32 * (fast ? 5 : 6);
+  return ((occ_words + 3) & ~size_t(3)) * 4 + static_cast<size_t>(warps) * 64 * 16 +
+         static_cast<size_t>(warps) * static_cast<size_t>(m.H) * 32 * (fast ? 5 : 6);
 }
 
 size_t mlp_smem_bytes(const DevModel& m) {
@@ -1199,10 +1203,10 @@ struct LaunchCfg {
   int sms = 148, per_sm = 1;
 };
 
-template <bool DEBUG, int LS, int FS, bool POW2, int VS>
+template <bool DEBUG, int LS, int FS, bool POW2, int VS, int TW>
 static cudaError_t launch_trace_t(const TraceParams& p, cudaStream_t st) {
-  auto kern = trace_encode_kernel<DEBUG, LS, FS, POW2, VS>;
-  const size_t smem = trace_smem_bytes(p.m);
+  auto kern = trace_encode_kernel<DEBUG, LS, FS, POW2, VS, TW>;
+  const size_t smem = trace_smem_bytes(p.m, TW);
   thread_local LaunchCfg cfg;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -1215,15 +1219,15 @@ static cudaError_t launch_trace_t(const TraceParams& p, cudaStream_t st) {
       if (e != cudaSuccess) return e;
     }
     cudaDeviceGetAttribute(&cfg.sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.per_sm, kern, 128, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.per_sm, kern, 32 * TW, smem);
     if (const char* c = std::getenv("LSNIF_TRACE_BLOCKS")) cfg.per_sm = std::min(cfg.per_sm, std::atoi(c));
     cfg.dev = dev;
     cfg.smem = smem;
   }
   const int sms = cfg.sms, per_sm = cfg.per_sm;
-  const int64_t nbatch = (p.n + 127) / 128;
-  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(nbatch, static_cast<int64_t>(sms) * std::max(per_sm, 1)));
-  kern<<<grid, 128, smem, st>>>(p);
+  const int64_t blocks = (p.n + 32 * TW - 1) / (32 * TW);  // one 32-ray batch per warp
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>(blocks, static_cast<int64_t>(sms) * std::max(per_sm, 1)));
+  kern<<<grid, 32 * TW, smem, st>>>(p);
   return cudaGetLastError();
 }
 
@@ -1231,8 +1235,13 @@ cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st) {
   if (p.n <= 0) return cudaSuccess;
   const bool fast = p.m.L == 2 && p.m.F == 3 && p.m.M_pow2 && p.m.V == 32;
   if (debug)
-    return fast ? launch_trace_t<true, 2, 3, true, 32>(p, st) : launch_trace_t<true, 0, 0, false, 0>(p, st);
-  return fast ? launch_trace_t<false, 2, 3, true, 32>(p, st) : launch_trace_t<false, 0, 0, false, 0>(p, st);
+    return fast ? launch_trace_t<true, 2, 3, true, 32, 8>(p, st) : launch_trace_t<true, 0, 0, false, 0, 8>(p, st);
+  if (!fast) return launch_trace_t<false, 0, 0, false, 0, 8>(p, st);
+  // many waves of 32-ray batches (>= 4 x the ~4.7k resident warps): 1024-thread
+  // blocks; a device-side count (scene / renderer queries) may be far below its
+  // upper bound p.n, so those keep the one-wave configuration
+  const bool big = !p.n_dev && p.n >= int64_t(4) * 4736 * 32;
+  return big ? launch_trace_t<false, 2, 3, true, 32, 32>(p, st) : launch_trace_t<false, 2, 3, true, 32, 8>(p, st);
 }
 
 template <int HID>
