@@ -57,8 +57,12 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
   // point pool per warp: entry t (fp32) and code (axis | plane << 2) in
   // separate arrays, H x 32 each (5 or 6 bytes per point)
   using code_t = typename std::conditional<(VS != 0 && VS < 64), uint8_t, uint16_t>::type;
-  float4* lane_ray = reinterpret_cast<float4*>(smem + ((occ_words + 3) & ~3)) + warp * 64;
-  float* pool_t = reinterpret_cast<float*>(smem + ((occ_words + 3) & ~3) + TW * 64 * 4) + warp * (H * 32);
+  // stop mask in SMEM: one bit per padded cell, or (1024-thread blocks, one
+  // per SM) one byte per cell, which turns the per-step test into a byte load
+  constexpr bool kByteMask = TW == 32;
+  const int mask_words = kByteMask ? (occ_words * 32 + 15) / 16 * 4 : (occ_words + 3) & ~3;
+  float4* lane_ray = reinterpret_cast<float4*>(smem + mask_words) + warp * 64;
+  float* pool_t = reinterpret_cast<float*>(smem + mask_words + TW * 64 * 4) + warp * (H * 32);
   code_t* pool_c = reinterpret_cast<code_t*>(pool_t - warp * (H * 32) + TW * H * 32) + warp * (H * 32);
   auto pool_put = [&](int i, uint2 e) {
     pool_t[i] = __uint_as_float(e.x);
@@ -102,7 +106,18 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
   issue_claim();
   int64_t next_wb = claimed();
   load_ray(next_wb);
-  for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.stop + i);
+  if (kByteMask) {
+    for (int i = threadIdx.x; i < occ_words * 8; i += blockDim.x) {  // 4 cells per 32-bit store
+      const uint32_t w = __ldg(m.stop + (i >> 3)) >> ((i & 7) * 4);
+      smem[i] = (w & 1u) | ((w & 2u) << 7) | ((w & 4u) << 14) | ((w & 8u) << 21);
+    }
+  } else {
+    for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.stop + i);
+  }
+  auto stop_at = [&](uint32_t idx) -> bool {
+    if (kByteMask) return reinterpret_cast<const uint8_t*>(smem)[idx] != 0;
+    return stop_bit(smem, idx);
+  };
   __syncthreads();
   while (next_wb < nwb) {
     const int64_t wbatch = next_wb;
@@ -130,7 +145,7 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
     int count = 0;
     bool fio = false;
     if (pair && walk_setup<VS>(m, o, d, t_min, w)) {
-      if (stop_bit(smem, w.idx)) {  // start cell (always inside the grid)
+      if (stop_at(w.idx)) {  // start cell (always inside the grid)
         fio = w.axis0 < 0;
         pool_put(lane, pack_point(w.t0, w.axis0, w.plane0));
         if (DEBUG) {
@@ -144,7 +159,7 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
       bool p1, p2;
       if (count < H) {
         while (walk_step(w, tn, p1, p2)) {
-          if (stop_bit(smem, w.idx)) {
+          if (stop_at(w.idx)) {
             // The crossed plane of the stepped axis (dda.cpp:89-95: c_new for
             // +steps, c_new + 1 for -steps) is the integer nearest to
             // V * (o + tn d) along that axis: tn is within a few ulps of the
@@ -1184,7 +1199,8 @@ cudaError_t compute_zero_hit(const DevModel& m, lsnif_hit* host_out) {
 size_t trace_smem_bytes(const DevModel& m, int warps) {
   const size_t occ_words = static_cast<size_t>(m.stop_words);
   const bool fast = m.L == 2 && m.F == 3 && m.M_pow2 && m.V == 32;  // 1-byte point codes
-  return ((occ_words + 3) & ~size_t(3)) * 4 + static_cast<size_t>(warps) * 64 * 16 +
+  const size_t mask_bytes = warps == 32 ? (occ_words * 32 + 15) / 16 * 16 : ((occ_words + 3) & ~size_t(3)) * 4;
+  return mask_bytes + static_cast<size_t>(warps) * 64 * 16 +
          static_cast<size_t>(warps) * static_cast<size_t>(m.H) * 32 * (fast ? 5 : 6);
 }
 
