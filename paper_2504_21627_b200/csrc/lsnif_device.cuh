@@ -257,6 +257,27 @@ __device__ __forceinline__ bool walk_step(Walk& w, float& tn, bool& p1, bool& p2
   return true;
 }
 
+// One advance of walk_step without its t1 test, for walks checked against a
+// stop mask whose padded border is all set: the t_next sequence of a walk is
+// non-decreasing, so the walk_step loop stops before a stop cell exactly when
+// that cell's entry t exceeds t1, and no cell in between emits; the caller
+// tests tn > t1 once per stop cell. Any moving walk reaches the border within
+// 3 (V + 2) advances; not for a walk with no moving axis (t1 = -inf).
+__device__ __forceinline__ void walk_advance(Walk& w, float& tn, bool& p1, bool& p2) {
+  p1 = w.tn[1] < w.tn[0];
+  tn = p1 ? w.tn[1] : w.tn[0];
+  p2 = w.tn[2] < tn;
+  tn = p2 ? w.tn[2] : tn;
+  const bool a0 = !p1 && !p2;
+  const bool a1 = p1 && !p2;
+  if (a0) w.tn[0] = __fadd_rn(w.tn[0], w.td[0]);
+  if (a1) w.tn[1] = __fadd_rn(w.tn[1], w.td[1]);
+  if (p2) w.tn[2] = __fadd_rn(w.tn[2], w.td[2]);
+  int dl = p1 ? w.lin[1] : w.lin[0];
+  dl = p2 ? w.lin[2] : dl;
+  w.idx += static_cast<uint32_t>(dl);
+}
+
 // Cell coordinates (unpadded, may be -1 or V when outside) of a padded index.
 template <int VS>
 __device__ __forceinline__ void walk_cell(const DevModel& m, uint32_t idx, int c[3]) {

@@ -157,9 +157,13 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
       }
       float tn;
       bool p1, p2;
-      if (count < H) {
-        while (walk_step(w, tn, p1, p2)) {
+      if (count < H && w.t1 != -__int_as_float(0x7f800000)) {
+        // one latch (the advance at the bottom) keeps this a single loop:
+        // lanes at a stop cell emit while the others keep walking
+        walk_advance(w, tn, p1, p2);
+        for (;;) {
           if (stop_at(w.idx)) {
+            if (tn > w.t1) break;  // the walk ended before this cell (dda.cpp:106)
             // The crossed plane of the stepped axis (dda.cpp:89-95: c_new for
             // +steps, c_new + 1 for -steps) is the integer nearest to
             // V * (o + tn d) along that axis: tn is within a few ulps of the
@@ -179,6 +183,7 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
             }
             if (++count >= H) break;  // first-H truncation (dda.cpp:99)
           }
+          walk_advance(w, tn, p1, p2);
         }
       }
     }
