@@ -1,5 +1,6 @@
 """Small end-to-end exercise of every kernel family for compute-sanitizer:
-query (trace + MLP; in-kernel clip, given pair intervals, host staging),
+query (trace + MLP; in-kernel clip, given pair intervals, host staging; one
+launch large enough for the 1024-thread / byte-mask trace configuration),
 debug traverse, infer_batch, scene query (device and host), render, and two
 training steps."""
 import os
@@ -19,6 +20,8 @@ rays = lsnif.rays_to_tensor(np.concatenate([W.camera_rays(64, 48), W.incoherent_
 gm.query(rays, lsnif.CLOSEST)
 gm.query(rays, lsnif.ANY)
 gm.debug_traverse(rays[:512])
+big = lsnif.rays_to_tensor(W.incoherent_rays(640 * 1024, gm.aabb, seed=5), "cuda")  # >= 4 waves: 1024-thread blocks
+gm.query(big, lsnif.CLOSEST)
 ivs = torch.rand((rays.shape[0], 2), device="cuda").sort(dim=1).values * 4  # given pair intervals
 gm.query_pairs(rays, ivs, lsnif.CLOSEST)
 gm.query_host(rays.cpu().numpy().view(lsnif.RAY_DTYPE).reshape(-1), lsnif.ANY)
