@@ -241,3 +241,19 @@ def test_non_finite_rays_do_not_disturb_others(gmodel):
     got = gmodel.query(lsnif.rays_to_tensor(mixed)).cpu().numpy()
     torch.cuda.synchronize()
     assert np.array_equal(np.concatenate([got[:7000], got[7000 + len(bad):]]), ref)
+
+
+def test_block_configurations_agree(gmodel):
+    """A launch of >= 4 waves runs the 1024-thread / byte-per-cell stop-mask
+    trace configuration, small launches the 256-thread / bit-mask one (whose
+    DDA is checked bit for bit against the oracle above): same rays, same
+    hits, bit for bit."""
+    rays = W.incoherent_rays(700_000, gmodel.aabb, seed=17)
+    t = lsnif.rays_to_tensor(rays)
+    big = gmodel.query(t).cpu().numpy()
+    small = torch.cat([gmodel.query(t[i:i + 87_500]) for i in range(0, len(rays), 87_500)]).cpu().numpy()
+    assert np.array_equal(big, small)
+    for mode in (lsnif.ANY,):
+        assert np.array_equal(gmodel.query(t, mode).cpu().numpy(),
+                              torch.cat([gmodel.query(t[i:i + 87_500], mode)
+                                         for i in range(0, len(rays), 87_500)]).cpu().numpy())
