@@ -430,6 +430,15 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
   m.w1_bytes = static_cast<uint32_t>(c1.size());
   m.w2_bytes = static_cast<uint32_t>(c2.size());
   m.w3_bytes = static_cast<uint32_t>(c3.size());
+  {  // X-tile ring depth: the deepest that fits the per-block SMEM opt-in limit
+    int dev = 0, optin = 0;
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    ck(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev), "cudaDeviceGetAttribute");
+    m.x_stages = lsnif_dev::mlp_x_stages(m, static_cast<size_t>(optin));
+    if (m.x_stages == 0)
+      fail(LSNIF_UNSUPPORTED, "input width H*L*F too large for the MLP kernel's shared memory at this hidden "
+                              "width (weights + two X tiles must fit one SM)");
+  }
 
   // Logits of the all-zero input (rays without boundary points), fp32 with
   // the reference's sequential order (renderer.cpp:197-207).

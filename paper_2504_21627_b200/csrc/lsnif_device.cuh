@@ -48,6 +48,7 @@ struct DevModel {
   const uint32_t* occ;                 // V^3/32 words
   const uint32_t* stop;                // (V+2)^3 bits: occupied cells + the outside border
   int stop_words;
+  int x_stages;                        // MLP X-tile ring depth (set at load from the SMEM budget)
   const uint2* tables[kMaxLevels];     // M entries x 4 binary16 (F <= 4, zero padded)
   int hidden, n_out, n_mat, N3;        // N3: layer-3 MMA width (>= n_out, multiple of 16)
   const uint8_t* w_canon;              // W1 | W2 | W3, UMMA K-major canonical fp16

@@ -104,7 +104,9 @@ cudaError_t launch_broad_phase(const DevModel& m, const InstanceParams& ip, cons
 cudaError_t launch_merge(const DevModel& m, const InstanceParams& ip, const lsnif_ray* rays,
                          const lsnif_hit* hits, const int32_t* slots, const int32_t* count, int64_t n_max,
                          int mode, lsnif_scene_hit* out, cudaStream_t st);
-size_t mlp_smem_bytes(const DevModel& m);
+size_t mlp_smem_bytes(const DevModel& m, int x_stages);
+// Deepest X ring (4..2 stages) whose SMEM fits smem_limit; 0 if none does.
+int mlp_x_stages(const DevModel& m, size_t smem_limit);
 cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st);
 cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st);
 cudaError_t launch_infer_f32(const DevModel& m, const float* x, int64_t n, const lsnif_interval* iv,

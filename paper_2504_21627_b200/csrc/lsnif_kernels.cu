@@ -457,13 +457,16 @@ extern "C" int lsnif_probe_mlp_timeline(unsigned long long* host, int n) {
 #define TL_STAMP(slot) (void)0
 #endif
 
-template <int HID>
+template <int HID, int NS>
 __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(const MlpParams P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   using Lay = MlpLayout<HID>;
   constexpr int K2 = Lay::kK2;
   constexpr int EW = Lay::kEpiWarps;
-  constexpr int NS = Lay::kXStages;
+  // NS: X ring depth, 4 or (inputs too wide for four stages next to the
+  // weights, mlp_x_stages) 2; a compile-time constant keeps the ring
+  // arithmetic off the issuing thread's critical path
+  static_assert(NS == 4 || NS == 2, "X ring depth");
   static_assert(HID == 128 || HID == 64, "hidden width 64 (low-quality LSNIF) or 128 (high-quality)");
   const DevModel& m = P.m;
   if (blockIdx.x == 0 && threadIdx.x == 0) TL_STAMP(1023 * 64 + 0);  // kernel entry
@@ -1209,11 +1212,17 @@ size_t trace_smem_bytes(const DevModel& m, int warps) {
          static_cast<size_t>(warps) * static_cast<size_t>(m.H) * 32 * (fast ? 5 : 6);
 }
 
-size_t mlp_smem_bytes(const DevModel& m) {
+size_t mlp_smem_bytes(const DevModel& m, int stages) {
   const size_t x = (static_cast<size_t>(kTileM) * m.K1P * 2 + 1023) & ~size_t(1023);
   // + barriers, TMEM slot, bin tile starts and the scaled b1 (1 KB tail)
   return 1024 + m.w1_bytes + m.w2_bytes + ((m.w3_bytes + 1023) & ~1023u) + kBinTileBytes +
-         MlpLayout<128>::kXStages * x + 1024 + 2 * MlpLayout<128>::kEpiWarps * 10 * 32 * 4;
+         static_cast<size_t>(stages) * x + 1024 + 2 * MlpLayout<128>::kEpiWarps * 10 * 32 * 4;
+}
+
+int mlp_x_stages(const DevModel& m, size_t smem_limit) {
+  if (mlp_smem_bytes(m, 4) <= smem_limit) return 4;
+  if (mlp_smem_bytes(m, 2) <= smem_limit) return 2;
+  return 0;
 }
 
 // Per-(kernel, device, smem size) launch configuration, computed once: the
@@ -1265,16 +1274,16 @@ cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st) {
   return big ? launch_trace_t<false, 2, 3, true, 32, 32>(p, st) : launch_trace_t<false, 2, 3, true, 32, 8>(p, st);
 }
 
-template <int HID>
+template <int HID, int NS>
 static cudaError_t launch_mlp_t(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st) {
-  const size_t smem = mlp_smem_bytes(p.m);
+  const size_t smem = mlp_smem_bytes(p.m, p.m.x_stages);
   const unsigned grid = static_cast<unsigned>(std::min(max_tiles, num_sms));
   thread_local LaunchCfg c;
   int dev = 0;
   cudaGetDevice(&dev);
   if (c.dev != dev || c.smem != smem) {
     cudaError_t e =
-        cudaFuncSetAttribute(mlp_tc_kernel<HID>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaFuncSetAttribute(mlp_tc_kernel<HID, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     c.dev = dev;
     c.smem = smem;
@@ -1289,13 +1298,16 @@ static cudaError_t launch_mlp_t(const MlpParams& p, int max_tiles, int num_sms, 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = attr;
   lc.numAttrs = 1;
-  return cudaLaunchKernelEx(&lc, mlp_tc_kernel<HID>, p);
+  return cudaLaunchKernelEx(&lc, mlp_tc_kernel<HID, NS>, p);
 }
 
 cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st) {
   if (max_tiles <= 0) return cudaSuccess;
-  if (p.m.hidden == 128) return launch_mlp_t<128>(p, max_tiles, num_sms, st);
-  if (p.m.hidden == 64) return launch_mlp_t<64>(p, max_tiles, num_sms, st);
+  const bool deep = p.m.x_stages >= 4;  // else the 2-stage ring (wide inputs)
+  if (p.m.hidden == 128)
+    return deep ? launch_mlp_t<128, 4>(p, max_tiles, num_sms, st) : launch_mlp_t<128, 2>(p, max_tiles, num_sms, st);
+  if (p.m.hidden == 64)
+    return deep ? launch_mlp_t<64, 4>(p, max_tiles, num_sms, st) : launch_mlp_t<64, 2>(p, max_tiles, num_sms, st);
   return cudaErrorNotSupported;
 }
 

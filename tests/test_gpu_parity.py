@@ -257,3 +257,46 @@ def test_block_configurations_agree(gmodel):
         assert np.array_equal(gmodel.query(t, mode).cpu().numpy(),
                               torch.cat([gmodel.query(t[i:i + 87_500], mode)
                                          for i in range(0, len(rays), 87_500)]).cpu().numpy())
+
+
+def shell_occupancy(V: int) -> np.ndarray:
+    """A thick spherical shell on a V^3 grid, packed as the model format
+    stores it (cell x + V (y + V z), bit i & 7 of byte i >> 3)."""
+    c = (np.arange(V) + 0.5) / V - 0.5
+    z, y, x = np.meshgrid(c, c, c, indexing="ij")
+    r = np.sqrt(x * x + y * y + z * z)
+    bits = ((r > 0.25) & (r < 0.42)).reshape(-1).astype(np.uint8)
+    return np.packbits(bits, bitorder="little")
+
+
+@pytest.mark.parametrize("V,H,levels,F,M,hidden,n_mat", [
+    (16, 12, [16, 48], 2, 50021, 64, 3),          # non-power-of-two M, F = 2
+    (64, 10, [64, 128, 192], 4, 1 << 15, 128, 1),  # V = 64 (36 KB bit mask), three levels, F = 4
+])
+def test_generic_configuration_parity(tmp_path, V, H, levels, F, M, hidden, n_mat):
+    """The generic trace instantiation (anything but V = 32, L = 2, F = 3,
+    power-of-two M): DDA points / t / cells, hash indices and fp32 features
+    bit-exact against the oracle, and the full query through the same gates
+    (SURVEY §8(a) A5-A9 at other model shapes)."""
+    from oracle import oracle as O
+    frame = np.array([-1.0, -0.5, -1.2, 1.1, 0.9, 1.0], np.float32)
+    om = O.OracleModel.random(shell_occupancy(V), V, H, levels, F, M, hidden, n_mat, frame, 7)
+    path = str(tmp_path / f"v{V}.lsnif")
+    om.save(path)
+    om = O.OracleModel.load(path)
+    gm = lsnif.GpuModel(path)
+    rays = np.concatenate([W.incoherent_rays(20000, gm.aabb, seed=23), edge_rays(gm.aabb)])
+    ref = om.trace(rays)
+    got = {k: v.cpu().numpy() for k, v in gm.debug_traverse(lsnif.rays_to_tensor(rays)).items()}
+    assert np.array_equal(got["info"], ref["info"])
+    for k in ("interval", "t", "pts", "feat"):
+        assert np.array_equal(got[k].view(np.uint32), ref[k].view(np.uint32)), k
+    assert np.array_equal(got["cells"].view(np.uint32), ref["cells"])
+    assert np.array_equal(got["hidx"].view(np.uint32), ref["hidx"])
+    assert (ref["info"] & 255).sum() > 1000
+    q = om.narrow_phase(rays, 0, 0)
+    g = lsnif.hits_to_numpy(gm.query(lsnif.rays_to_tensor(rays)))
+    span = ref["interval"][:, 1] - ref["interval"][:, 0]
+    vis, mat, both, dt = compare_query(g, q, f"V{V}")
+    assert vis >= 0.999 and mat >= 0.999, (vis, mat)
+    assert np.all(dt[both] <= 2e-3 * span[both] + 1e-6)
