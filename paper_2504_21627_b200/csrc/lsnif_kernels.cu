@@ -1270,7 +1270,9 @@ cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st) {
   // many waves of 32-ray batches (>= 4 x the ~4.7k resident warps): 1024-thread
   // blocks; a device-side count (scene / renderer queries) may be far below its
   // upper bound p.n, so those keep the one-wave configuration
-  const bool big = !p.n_dev && p.n >= int64_t(4) * 4736 * 32;
+  // (and only while its SMEM - byte mask + 32 warps' pools - fits the 227 KB
+  // per-block opt-in limit: a hit cap H above ~26 does not)
+  const bool big = !p.n_dev && p.n >= int64_t(4) * 4736 * 32 && trace_smem_bytes(p.m, 32) <= 232448;
   return big ? launch_trace_t<false, 2, 3, true, 32, 32>(p, st) : launch_trace_t<false, 2, 3, true, 32, 8>(p, st);
 }
 

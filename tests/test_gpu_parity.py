@@ -300,3 +300,32 @@ def test_generic_configuration_parity(tmp_path, V, H, levels, F, M, hidden, n_ma
     vis, mat, both, dt = compare_query(g, q, f"V{V}")
     assert vis >= 0.999 and mat >= 0.999, (vis, mat)
     assert np.all(dt[both] <= 2e-3 * span[both] + 1e-6)
+
+
+def test_fast_path_max_hit_cap_large_launch(tmp_path, oracle_teapot):
+    """The fast trace shape (V = 32, L = 2, F = 3, power-of-two M) at the
+    largest hit cap (H = 32, input width 192: the MLP's 2-stage X ring) in a
+    launch big enough for the 1024-thread configuration, whose SMEM would not
+    fit at this H (the launcher keeps 256-thread blocks): results equal the
+    sliced (small-launch) query and the oracle's traversal."""
+    from oracle import oracle as O
+    om = O.OracleModel.random(oracle_teapot.occupancy(), 32, 32, oracle_teapot.level_res, 3,
+                              oracle_teapot.M, 128, 2, oracle_teapot.aabb, 11)
+    path = str(tmp_path / "h32.lsnif")
+    om.save(path)
+    om = O.OracleModel.load(path)
+    gm = lsnif.GpuModel(path)
+    rays = W.incoherent_rays(700_000, gm.aabb, seed=29)
+    t = lsnif.rays_to_tensor(rays)
+    big = gm.query(t).cpu().numpy()
+    small = torch.cat([gm.query(t[i:i + 87_500]) for i in range(0, len(rays), 87_500)]).cpu().numpy()
+    assert np.array_equal(big, small)
+    sub = rays[:20000]
+    ref = om.trace(sub)
+    got = {k: v.cpu().numpy() for k, v in gm.debug_traverse(lsnif.rays_to_tensor(sub)).items()}
+    assert np.array_equal(got["info"], ref["info"])
+    assert np.array_equal(got["t"].view(np.uint32), ref["t"].view(np.uint32))
+    assert np.array_equal(got["feat"].view(np.uint32), ref["feat"].view(np.uint32))
+    q = om.narrow_phase(sub, 0, 0)
+    vis, mat, both, dt = compare_query(lsnif.hits_to_numpy(gm.query(lsnif.rays_to_tensor(sub))), q, "H32")
+    assert vis >= 0.999 and mat >= 0.999, (vis, mat)
