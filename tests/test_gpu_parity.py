@@ -272,6 +272,7 @@ def shell_occupancy(V: int) -> np.ndarray:
 @pytest.mark.parametrize("V,H,levels,F,M,hidden,n_mat", [
     (16, 12, [16, 48], 2, 50021, 64, 3),          # non-power-of-two M, F = 2
     (64, 10, [64, 128, 192], 4, 1 << 15, 128, 1),  # V = 64 (36 KB bit mask), three levels, F = 4
+    (32, 16, [32, 64, 96, 128], 4, 1 << 16, 64, 8),  # the limits: L = 4, L F = 16, H L F = 256, n_mat = 8
 ])
 def test_generic_configuration_parity(tmp_path, V, H, levels, F, M, hidden, n_mat):
     """The generic trace instantiation (anything but V = 32, L = 2, F = 3,
