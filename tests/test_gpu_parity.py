@@ -330,3 +330,24 @@ def test_fast_path_max_hit_cap_large_launch(tmp_path, oracle_teapot):
     q = om.narrow_phase(sub, 0, 0)
     vis, mat, both, dt = compare_query(lsnif.hits_to_numpy(gm.query(lsnif.rays_to_tensor(sub))), q, "H32")
     assert vis >= 0.999 and mat >= 0.999, (vis, mat)
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 33, 127, 129, (1 << 21) - 1, (1 << 21) + 1])
+def test_batch_and_chunk_boundaries(gmodel, oracle_teapot, n):
+    """Ray counts at the edges of 32-ray warp batches, 128-row MLP tiles and
+    2^21-ray launch chunks (and the empty query): every result equals the
+    same rays answered inside a larger batch, bit for bit, and the pair /
+    visibility flags equal the oracle's on a sample."""
+    pool = W.incoherent_rays(max(n, 1) + 1000, gmodel.aabb, seed=31)
+    rays = pool[1000:1000 + n]
+    t_all = lsnif.rays_to_tensor(pool)
+    ref = gmodel.query(t_all).cpu().numpy()[1000:1000 + n]
+    got = gmodel.query(lsnif.rays_to_tensor(rays) if n else t_all[:0]).cpu().numpy()
+    assert got.shape == (n, 8)
+    assert np.array_equal(got, ref)
+    host = gmodel.query_host(rays) if n else None
+    if n:
+        assert host.view(np.int32).reshape(-1, 8).tobytes() == ref.tobytes()
+        k = min(n, 4096)
+        q = oracle_teapot.narrow_phase(rays[:k], 0, 0)
+        assert np.array_equal(got[:k, 0].view(np.uint32) & 1, q["flags_material"] & 1)
