@@ -89,3 +89,32 @@ def test_scene_query_host_matches_device(scenes, n, mode):
     out = torch.empty((n, 16), dtype=torch.int32).pin_memory()
     gs.query_host(pin, mode, out=out)
     assert np.array_equal(out.numpy(), dev)
+
+
+def test_scene_more_instances_than_side_streams(scenes):
+    """11 instances (more than the 8 side streams; instance k on stream k % 8)
+    and an empty scene: the merged hits follow the oracle's object-order rules."""
+    gs, om, w2o, O = scenes
+    gm = [lsnif.GpuModel(os.path.join(GOLD, n + ".lsnif")) for n in W.C4_MODELS]
+    oms = [O.OracleModel.load(os.path.join(GOLD, n + ".lsnif")) for n in W.C4_MODELS]
+    n_inst = 11
+    idx = [k % len(gm) for k in range(n_inst)]
+    xf = []
+    for k in range(n_inst):  # identity rotation, instances spread on a line with overlap
+        m = np.zeros((3, 4), np.float32)
+        m[:, :3] = np.eye(3)
+        m[:, 3] = -np.array([1.3 * k - 6.5, 0.2 * (k % 3), 0.0], np.float32)
+        xf.append(m)
+    scene = lsnif.GpuScene([(gm[idx[k]], xf[k]) for k in range(n_inst)])
+    box = np.array([-8.0, -2.0, -2.0, 8.0, 2.0, 2.0], np.float32)
+    rays = W.incoherent_rays(30000, box, seed=41)
+    for mode in (0, 1):
+        ref = O.scene_query([oms[i] for i in idx], xf, rays, mode, 0)
+        got = lsnif.scene_hits_to_numpy(scene.query(lsnif.rays_to_tensor(rays), mode))
+        assert np.mean(got["flags"] == ref["flags"]) >= 0.999
+        assert np.mean(got["object_index"] == ref["object_index"]) >= 0.999
+        assert (ref["flags"] == 1).sum() > 100
+    empty = lsnif.GpuScene([])
+    e = lsnif.scene_hits_to_numpy(empty.query(lsnif.rays_to_tensor(rays[:100]), 0))
+    assert np.all(e["flags"] == 0) and np.all(e["object_index"] == -1)
+    assert np.array_equal(e["t"], rays["t_max"][:100])
