@@ -7,6 +7,8 @@ the same rays and the same model file. Gates:
     of MLP rays; for rays both call occluded |dt| <= 2e-3*(exit-enter),
     normal angle <= 1 deg, |d albedo| <= 2e-3.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -351,3 +353,18 @@ def test_batch_and_chunk_boundaries(gmodel, oracle_teapot, n):
         k = min(n, 4096)
         q = oracle_teapot.narrow_phase(rays[:k], 0, 0)
         assert np.array_equal(got[:k, 0].view(np.uint32) & 1, q["flags_material"] & 1)
+
+
+def test_cpp_adapter_example_runs():
+    """examples/query_cpp (the C++ adapter: Model::load, intersect,
+    infer_pairs, Scene + render) runs against the in-tree library."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "query_cpp")
+    if not os.path.exists(exe):
+        pytest.skip("examples/query_cpp not built (make)")
+    out = subprocess.run([exe, os.path.join(root, "tests", "golden", "teapot_seed0.lsnif")],
+                         capture_output=True, text=True, timeout=120, cwd=root)
+    assert out.returncode == 0, out.stderr
+    assert "rays accepted a neural hit" in out.stdout
+    assert "infer_pairs:" in out.stdout and "render 64x36x2" in out.stdout
