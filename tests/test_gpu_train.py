@@ -118,3 +118,25 @@ def test_box_labels_geometric_normals(setup):
     occ = got["occluded"] != 0
     n = got["normal"][occ]
     assert np.allclose(np.abs(n).max(axis=1), 1.0)  # box normals are axis-aligned
+
+
+@pytest.mark.parametrize("batch", [1, 999])
+def test_odd_batch_sizes(setup, batch):
+    """Batches that are not multiples of the warp / tile sizes: labels and the
+    batch gradients still match the oracle."""
+    O, om, mesh = setup
+    tr = lsnif.Trainer(INIT, mesh, batch=batch, seed=13)
+    rays, tg = tr.sample(step=2, n=batch)
+    K1 = om.H * om.n_levels * om.F
+    hid, n_out = om.hidden, 8 + om.n_mat
+    n_mlp = hid * K1 + hid + hid * hid + hid + n_out * hid + n_out
+    n_tab = om.n_levels * om.M * om.F
+    loss, g_mlp, g_tab = tr.batch_grad(rays, tg, n_mlp, n_tab)
+    ref_loss, ref_mlp, ref_tab = O.train_batch_grad(om, rays.cpu().numpy().view(O.RAY_DTYPE).reshape(-1),
+                                                    targets_np(tg))
+    assert abs(loss["total"] - ref_loss[0]) <= 1e-4 * max(abs(ref_loss[0]), 1e-6)
+    g = g_mlp.cpu().numpy()
+    assert np.linalg.norm(g - ref_mlp) <= 1e-4 * max(np.linalg.norm(ref_mlp), 1e-30)
+    gt = g_tab.cpu().numpy()
+    assert np.linalg.norm(gt - ref_tab) <= 1e-4 * max(np.linalg.norm(ref_tab), 1e-30)
+    tr.step(2)  # the full step loop at this batch size
