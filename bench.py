@@ -278,8 +278,14 @@ def time_cpu(O, model, primary, shadow, target_s: float):
     frac = min(1.0, target_s * est / total)
     p1, s1, step = cpu_sample(primary, shadow, frac)
     # when the whole workload is shorter than the target, time best-of-reps
-    # passes so the measurement still spans ~target_s of CPU work
-    reps = max(1, int(round(target_s * est / max(len(p1) + len(s1), 1))))
+    # passes so the measurement still spans ~target_s of CPU work (reps from
+    # one measured pass of the sample, not the small-probe estimate)
+    t0 = time.perf_counter()
+    model.narrow_phase(p1, 0, 0)
+    if len(s1):
+        model.narrow_phase(s1, 1, 0)
+    one = max(time.perf_counter() - t0, 1e-6)
+    reps = max(1, min(200, int(round(target_s / one))))
     tp = model.time_narrow_phase(p1, 0, 0, reps)
     ts = model.time_narrow_phase(s1, 1, 0, reps) if len(s1) else 0.0
     n = len(p1) + len(s1)
