@@ -17,7 +17,10 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <type_traits>
+#include <utility>
 
 #include "lsnif_device.cuh"
 #include "lsnif_internal.hpp"
@@ -1225,6 +1228,24 @@ int mlp_x_stages(const DevModel& m, size_t smem_limit) {
   return 0;
 }
 
+// Raise (never lower) a kernel's dynamic-SMEM limit on the current device:
+// host threads launching the same kernel for models of different sizes must
+// not shrink it under each other between the attribute call and the launch.
+template <typename K>
+static cudaError_t ensure_smem(K kern, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> granted;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = granted[{reinterpret_cast<const void*>(kern), dev}];
+  if (smem <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess) cur = smem;
+  return e;
+}
+
 // Per-(kernel, device, smem size) launch configuration, computed once: the
 // attribute and occupancy queries cost microseconds of host time per call.
 struct LaunchCfg {
@@ -1241,8 +1262,7 @@ static cudaError_t launch_trace_t(const TraceParams& p, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
   if (cfg.dev != dev || cfg.smem != smem) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = ensure_smem(kern, smem);
     if (e != cudaSuccess) return e;
     if (const char* c = std::getenv("LSNIF_TRACE_CARVEOUT")) {  // A/B probe: shared-memory share (%)
       e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(c));
@@ -1284,8 +1304,7 @@ static cudaError_t launch_mlp_t(const MlpParams& p, int max_tiles, int num_sms, 
   int dev = 0;
   cudaGetDevice(&dev);
   if (c.dev != dev || c.smem != smem) {
-    cudaError_t e =
-        cudaFuncSetAttribute(mlp_tc_kernel<HID, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaError_t e = ensure_smem(mlp_tc_kernel<HID, NS>, smem);
     if (e != cudaSuccess) return e;
     c.dev = dev;
     c.smem = smem;

@@ -113,3 +113,35 @@ def test_concurrent_scene_queries():
         return fn
 
     run_threads([worker(k) for k in range(len(sets))])
+
+
+def test_concurrent_models_of_different_shapes(setup, tmp_path):
+    """Host threads querying models whose kernels need different dynamic
+    SMEM (the teapot's 18-point pools and a V = 64 model's 36 KB bit mask) on
+    their own streams: the per-kernel SMEM limit is only ever raised, so no
+    thread's launch is invalidated by another's attribute call."""
+    from oracle import oracle as O
+    gm, sets = setup
+    occ = np.packbits((np.random.default_rng(5).random(64 ** 3) < 0.08).astype(np.uint8), bitorder="little")
+    om = O.OracleModel.random(occ, 64, 24, [64, 128], 3, 1 << 16, 128, 2,
+                              np.array([-1, -1, -1, 1, 1, 1], np.float32), 3)
+    path = str(tmp_path / "v64.lsnif")
+    om.save(path)
+    g64 = lsnif.GpuModel(path)
+    models = [gm, g64]
+    rays = [W.incoherent_rays(60000, m.aabb, seed=50 + k) for k, m in enumerate(models)]
+    ref = [m.query(lsnif.rays_to_tensor(r)).cpu().numpy() for m, r in zip(models, rays)]
+
+    def worker(k):
+        def fn():
+            s = torch.cuda.Stream()
+            ds = [lsnif.rays_to_tensor(r) for r in rays]
+            torch.cuda.current_stream().synchronize()
+            with torch.cuda.stream(s):
+                outs = [models[(k + it) % 2].query(ds[(k + it) % 2], stream=s) for it in range(8)]
+                s.synchronize()
+            for it, o in enumerate(outs):
+                assert np.array_equal(o.cpu().numpy(), ref[(k + it) % 2]), (k, it)
+        return fn
+
+    run_threads([worker(k) for k in range(4)])
