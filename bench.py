@@ -636,14 +636,23 @@ def main():
         stats_s = model.last_stats()
     n_step = len(primary) + len(shadow)
     gathered = {}
+    gather_out, gather_sizes = None, None
+    if strong and world > 1:  # C5: every rank's band size is known from the partition
+        from paper_2504_21627_b200.dist import ray_range
+        gather_sizes = [ray_range(3840 * 2160 * 16, world, r)[1] - ray_range(3840 * 2160 * 16, world, r)[0]
+                        for r in range(world)]
+        if rank == 0:
+            gather_out = torch.empty((sum(gather_sizes), 8), dtype=torch.int32,
+                                     device=dev if not gloo else "cpu")
 
     def step():
         model.query(d_primary, mode_p, out=d_hits_p)
         if d_shadow is not None:
             model.query(d_shadow, lsnif.ANY, out=d_hits_s)
-        if strong and world > 1:  # the one collective: result gather to rank 0
+        if strong and world > 1:  # the one collective: result gather to rank 0 (preallocated)
             from paper_2504_21627_b200.dist import gather_to_rank0
-            gathered["hits"] = gather_to_rank0(d_hits_p if not gloo else d_hits_p.cpu())
+            gathered["hits"] = gather_to_rank0(d_hits_p if not gloo else d_hits_p.cpu(),
+                                               out=gather_out, sizes=gather_sizes)
 
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):

@@ -22,24 +22,36 @@ def ray_range(n: int, world: int, rank: int) -> tuple[int, int]:
     return row_band(n, world, rank)
 
 
-def gather_to_rank0(local, group=None):
+def gather_to_rank0(local, group=None, out=None, sizes=None):
     """Gathers per-rank result tensors (first dim = rays, possibly unequal)
     into rank 0 in rank order; returns the concatenation on rank 0, None
-    elsewhere. Uses all_gather of padded equal-size buffers (one collective
-    for the sizes, one for the payload)."""
+    elsewhere. Point-to-point: every rank sends its band straight into its
+    slice of rank 0's output (one batched isend / irecv set, NCCL or gloo),
+    so no rank receives the other bands and nothing is re-concatenated.
+    `sizes` (per-rank row counts, e.g. from row_band) skips the size
+    exchange; `out` (rank 0, shape (sum(sizes),) + local.shape[1:]) is
+    filled in place, so a caller that preallocates it keeps allocations out
+    of its timed loop."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    n = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    sizes = [int(s.item()) for s in sizes]
-    cap = max(sizes)
-    pad = torch.zeros((cap,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    pad[: local.shape[0]] = local
-    bufs = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(bufs, pad, group=group)
+    if sizes is None:
+        n = torch.tensor([local.shape[0]], dtype=torch.int64, device=local.device)
+        gathered = [torch.zeros_like(n) for _ in range(world)]
+        dist.all_gather(gathered, n, group=group)
+        sizes = [int(x.item()) for x in gathered]
     if rank != 0:
+        if sizes[rank]:
+            dist.batch_isend_irecv([dist.P2POp(dist.isend, local.contiguous(), 0, group)])[0].wait()
         return None
-    return torch.cat([b[:s] for b, s in zip(bufs, sizes)])
+    if out is None:
+        out = torch.empty((sum(sizes),) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    offs = [0]
+    for x in sizes:
+        offs.append(offs[-1] + x)
+    out[offs[0]:offs[1]].copy_(local)
+    ops = [dist.P2POp(dist.irecv, out[offs[r]:offs[r + 1]], r, group) for r in range(1, world) if sizes[r]]
+    for req in (dist.batch_isend_irecv(ops) if ops else []):
+        req.wait()
+    return out

@@ -1,8 +1,9 @@
 """world_size-2 gloo test of the multi-GPU host path: each rank answers its
 row band of a camera frame (here with the CPU oracle standing in for the GPU
 kernels, which this container lacks) and the results are gathered to rank 0
-with the same gather the bench uses; the gathered frame must equal the
-single-process frame bit for bit."""
+with the same gather the bench uses (point-to-point into rank 0's output,
+with and without known sizes / a preallocated output); the gathered frame
+must equal the single-process frame bit for bit."""
 import os
 import socket
 
@@ -36,8 +37,15 @@ def _worker(rank, world, port, out_path):
     hits = m.narrow_phase(rays, 0, 1)
     t = torch.from_numpy(hits.view(np.int32).reshape(-1, 8).copy())
     full = D.gather_to_rank0(t)
+    # the bench's form: sizes known from the partition, output preallocated on rank 0
+    sizes = [(lambda b: (b[1] - b[0]) * W_)(D.row_band(H_, world, r)) for r in range(world)]
+    pre = torch.full((sum(sizes), 8), -7, dtype=torch.int32) if rank == 0 else None
+    again = D.gather_to_rank0(t, out=pre, sizes=sizes)
     if rank == 0:
+        assert again is pre and torch.equal(again, full)
         np.save(out_path, full.numpy())
+    else:
+        assert full is None and again is None
     dist.barrier()
     dist.destroy_process_group()
 
