@@ -4,16 +4,23 @@
 Metric (BASELINE.json): LSNIF ray queries/sec, one query = one input ray
 answered (including rays that miss the frame box).
 
-Default workload (configs[1], "C2"): the teapot LSNIF fixture
-(tests/golden/teapot_seed0.lsnif: reference train() setup state, seed 0),
-1920x1080 pixel-centre camera rays answered with the closest-hit rule, plus
-one NEE shadow ray per accepted primary hit answered with the any-hit rule.
-A step = the primary query + the shadow query. Under torchrun each rank
-answers its own frame (per-GPU work fixed: weak scaling, no data-path
-collective); the timed region is max-reduced over ranks.
+Default workload (configs[4], "C5", the north-star configuration): the teapot
+LSNIF fixture (tests/golden/teapot_seed0.lsnif: reference train() setup
+state, seed 0), 3840x2160 x 16 spp = 132,710,400 incoherent rays keyed by
+(pixel, sample), answered with the closest-hit rule (run_narrow_phase,
+renderer.cpp:232-265). The frame is split into contiguous row bands, one per
+GPU (strong scaling); every rank regenerates its own band from the
+index-addressable generator and answers it in pieces, and each finished
+piece is sent point-to-point into rank 0's full-frame result on a side
+stream while the next piece computes (NCCL over NVLink, the one collective,
+inside the timed step). Results are the packed 16 B wire records
+(lsnif_hit_wire). At N = 1 the same frame runs on one GPU.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c1]
-  python bench.py --impl reference   # the reference's CPU algorithm (oracle port)
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5|c3|c2|c1|c4|render]
+  python bench.py --impl reference   # the reference's CPU algorithm on the same rays
+
+`--gpus N` with N > 1 outside torchrun relaunches itself under
+torch.distributed.run with N ranks; under torchrun WORLD_SIZE must equal N.
 """
 from __future__ import annotations
 
@@ -36,11 +43,21 @@ METRIC = "LSNIF ray queries/sec at 1/2/4/8 B200, % of roofline, vs CPU ref (core
 UNIT = "rays/s"
 L2_FLUSH_BYTES = 256 << 20
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+C5_RAYS = 3840 * 2160 * 16
+C5_SEED = 5
+C5_CPU_STRIDE = 64          # CPU sample of C5: every 64th ray (2,073,600 rays), both CPU arms
+C5_PIECES = 8               # compute / gather pieces per band at N > 1
 
 WORKLOADS = {
+    "c5": "C5 (configs[4]): teapot LSNIF, 3840x2160 x 16 spp incoherent rays (132,710,400, "
+          "keyed by (pixel, sample): origins uniform in the frame box, directions uniform on S^2, "
+          "seed 5), closest-hit, packed 16 B results; contiguous row bands, one per GPU, each band "
+          "answered in 8 pieces whose results go point-to-point (NCCL) into rank 0's full-frame "
+          "buffer while the next piece computes (strong scaling)",
     "c2": "C2 (configs[1]): teapot LSNIF (seed-0 reference init), 1920x1080 pixel-centre "
           "primary rays (closest-hit) + NEE shadow rays toward a point light from the "
-          "accepted primary hits (any-hit), one frame per GPU",
+          "CPU reference's accepted primary hits (any-hit; the same shadow set for every arm), "
+          "one frame per GPU",
     "c3": "C3 (configs[2]): teapot LSNIF, 16,777,216 incoherent rays (origins uniform in "
           "the frame box, directions uniform on S^2, seed 3), closest-hit, per GPU",
     "c1": "C1 (configs[0]): teapot LSNIF, 256x256 pixel-centre primary rays, closest-hit",
@@ -51,41 +68,71 @@ WORKLOADS = {
               "glossy lid, glossy sphere, box, torus; point + sphere light, environment), "
               "1280x720 x 4 spp, 4 bounces, PrimaryMode::lsnif; rays = intersect_scene + "
               "occluded_batch queries issued by the renderer",
-    "c5": "C5 (configs[4]): teapot LSNIF, 3840x2160 x 16 spp incoherent rays (132,710,400, "
-          "keyed by (pixel, sample)), closest-hit, row bands tile-sharded across the GPUs with "
-          "an NCCL result gather to rank 0 inside the step (strong scaling)",
 }
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=list(WORKLOADS), default="c2")
+    ap.add_argument("--workload", choices=list(WORKLOADS), default="c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0,
-                    help="target CPU work per timed baseline pass")
+                    help="target CPU work per timed baseline measurement")
+    ap.add_argument("--rays", type=int, default=0,
+                    help="C5 frame size override (tests only; the line then says so)")
+    ap.add_argument("--dump", default="",
+                    help="(tests) rank 0 saves the gathered C5 frame (wire records) to this .npy")
     ap.add_argument("--dist-backend", default=os.environ.get("LSNIF_DIST_BACKEND", "nccl"),
                     help="nccl (one GPU per rank) or gloo (test mode: all ranks on cuda:0)")
     return ap.parse_args()
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`--gpus N` (N > 1) from a plain `python bench.py`: run the same command
+    as N ranks under torch.distributed.run (one process per GPU)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 # ----------------------------------------------------------------- workload
 
 def build_rays(workload: str, rank: int, box: np.ndarray, world: int = 1):
-    """Primary rays of one rank (before shadow generation)."""
+    """Primary rays of one rank (C1-C3; C5 is generated straight into pinned memory)."""
     from paper_2504_21627_b200 import workloads as W
-    from paper_2504_21627_b200.dist import ray_range
-    if workload == "c5":
-        s, e = ray_range(3840 * 2160 * 16, world, rank)
-        return W.incoherent_rays(e - s, box, seed=5, start=s)
     if workload == "c2":
         return W.camera_rays(1920, 1080, jitter=W.rank_jitter(rank))
     if workload == "c1":
         return W.camera_rays(256, 256, jitter=W.rank_jitter(rank))
-    return W.incoherent_rays(1 << 24, box, seed=3, start=rank << 24)
+    out = np.empty(1 << 24, W.RAY_DTYPE)
+    return W.incoherent_rays_into(out, box, 3, rank << 24)
+
+
+def c2_shadow_set(primary: np.ndarray, box):
+    """The C2 shadow rays, derived ONCE from the CPU reference's own primary
+    hits (oracle narrow phase on the whole frame): every arm answers exactly
+    the same rays (the GPU's fp16 MLP may accept a few different primaries)."""
+    from paper_2504_21627_b200 import workloads as W
+    O = cpu_oracle(True)
+    om = O.OracleModel.load(MODEL_PATH, fast=True)
+    hits = om.narrow_phase(primary, 0, 0)
+    return W.shadow_rays(primary, hits, box)[0]
+
+
+def c5_sample(box, total: int = C5_RAYS) -> tuple[np.ndarray, np.ndarray]:
+    """The CPU arms' C5 sample: every C5_CPU_STRIDE-th ray of the frame (the
+    GPU answers the same rays at the same indices)."""
+    from paper_2504_21627_b200 import workloads as W
+    idx = np.arange(0, total, C5_CPU_STRIDE, dtype=np.uint64)
+    return idx, W.incoherent_rays_at(idx, box, seed=C5_SEED)
 
 
 def load_peaks():
@@ -97,15 +144,6 @@ def load_peaks():
         return d
     except Exception:
         return dict(FALLBACK_PEAKS)
-
-
-def load_traffic(workload: str):
-    p = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
-    try:
-        with open(p) as f:
-            return json.load(f)
-    except Exception:
-        return {}
 
 
 def load_json(name: str):
@@ -139,12 +177,6 @@ def aux_rooflines(workload: str, trace_rays_per_s: float, sm_mhz, pts_per_ray: f
             l2 = json.loads(f.readline())
     except Exception:
         pass
-    if l2 and km:
-        rd = km["l2_read_bytes_per_ray"] * trace_rays_per_s / 1e9
-        out["l2_read"] = {"kernel": "trace_encode_kernel", "achieved": rd, "peak": l2["l2_stream_read_GBps"],
-                          "unit": "GB/s", "frac": rd / l2["l2_stream_read_GBps"],
-                          "source": "ncu L2 read sectors per ray (rays, tables, occupancy) x live rays/s; "
-                                    "peak = measured streaming L2 read bandwidth"}
     if l2:
         g = (8.0 * pts_per_ray + 8.0 * vol_per_ray) * trace_rays_per_s
         peak = l2["gather8_Gloads_per_s"] * 1e9
@@ -214,14 +246,14 @@ class ClockSampler:
 # ------------------------------------------------------------ CPU baseline
 
 def path_roofline(rays_per_s_gpu: float, n: int, rows: int, pts: int, vol: int, mlp_flops: float,
-                  peaks: dict) -> dict:
+                  peaks: dict, result_bytes: int = 32) -> dict:
     """SURVEY §8(d) whole-path ceiling per GPU: R_tensor = dense fp16 peak /
-    FLOP_ray, R_mem = HBM peak / B_ray (B_ray = 32 B ray + 32 B result + 48 B
-    per boundary point + 48 B per volume point), R_path = min of the two;
-    the path is issue/latency bound in traversal and encode, so this fraction
-    is small by construction (the per-kernel rooflines explain it)."""
+    FLOP_ray, R_mem = HBM peak / B_ray (B_ray = 32 B ray + the result record
+    + 48 B per boundary point + 48 B per volume point), R_path = min of the
+    two; the path is issue/latency bound in traversal and encode, so this
+    fraction is small by construction (the per-kernel rooflines explain it)."""
     flop_ray = mlp_flops / max(n, 1)
-    bytes_ray = 64.0 + 48.0 * (pts + vol) / max(n, 1)
+    bytes_ray = 32.0 + result_bytes + 48.0 * (pts + vol) / max(n, 1)
     tflops = peaks.get("bf16_tflops_sustained", 1400.0)
     r_tensor = tflops * 1e12 / max(flop_ray, 1e-9)
     r_mem = peaks["hbm_gbs"] * 1e9 / bytes_ray
@@ -243,13 +275,14 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_detail(rate: float, cores: int, mlp_rows_per_ray: float, hidden: int, k1: int, n_out: int) -> dict:
-    """rays/s per core, the CPU model, and the CPU MLP GFLOP/s
-    (rows with >= 1 point x 2 (K1 H + H^2 + H n_out) FLOP) so the CPU GEMV is
-    visibly not a strawman."""
+def cpu_detail(rate: float, cores: int, pairs_per_ray: float, hidden: int, k1: int, n_out: int) -> dict:
+    """rays/s per core, the CPU model, and the CPU MLP GFLOP/s.
+    The CPU reference runs its MLP (infer_batch, renderer.cpp:193-209) on
+    every pair (ray overlapping the frame box), points or not, so the CPU's
+    FLOP rate counts pairs x 2 (K1 H + H^2 + H n_out)."""
     flop_row = 2 * (k1 * hidden + hidden * hidden + hidden * n_out)
     return {"per_core": rate / max(cores, 1), "cpu_model": cpu_model(),
-            "mlp_gflops": rate * mlp_rows_per_ray * flop_row / 1e9}
+            "mlp_gflops": rate * pairs_per_ray * flop_row / 1e9}
 
 
 def cpu_oracle(fast: bool = True):
@@ -259,87 +292,103 @@ def cpu_oracle(fast: bool = True):
     return O
 
 
-def cpu_sample(primary: np.ndarray, shadow: np.ndarray, frac: float):
-    """Strided subsample of both ray sets (keeps the image-space mix)."""
-    step = max(1, int(round(1.0 / max(frac, 1e-9))))
-    return primary[::step], shadow[::step], step
-
-
-def time_cpu(O, model, primary, shadow, target_s: float):
-    """Times the oracle narrow phase (all host threads) on a sample of the
-    same workload sized for ~target_s of CPU work. Returns rays/s and info."""
-    total = len(primary) + len(shadow)
-    p0, s0, _ = cpu_sample(primary, shadow, 8192.0 / total)
+def time_cpu_sets(model, sets, target_s: float):
+    """Times the CPU reference narrow phase (all host threads) over the ray
+    sets [(rays, mode), ...] answered back to back: one untimed pass, then
+    repeated passes (best of) spanning ~target_s of CPU work. Returns
+    (rays/s, info)."""
+    n = sum(len(r) for r, _ in sets)
     t0 = time.perf_counter()
-    model.narrow_phase(p0, 0, 0)
-    if len(s0):
-        model.narrow_phase(s0, 1, 0)
-    est = (len(p0) + len(s0)) / max(time.perf_counter() - t0, 1e-6)
-    frac = min(1.0, target_s * est / total)
-    p1, s1, step = cpu_sample(primary, shadow, frac)
-    # when the whole workload is shorter than the target, time best-of-reps
-    # passes so the measurement still spans ~target_s of CPU work (reps from
-    # one measured pass of the sample, not the small-probe estimate)
-    t0 = time.perf_counter()
-    model.narrow_phase(p1, 0, 0)
-    if len(s1):
-        model.narrow_phase(s1, 1, 0)
+    for r, mode in sets:
+        if len(r):
+            model.narrow_phase(r, mode, 0)
     one = max(time.perf_counter() - t0, 1e-6)
     reps = max(1, min(200, int(round(target_s / one))))
-    tp = model.time_narrow_phase(p1, 0, 0, reps)
-    ts = model.time_narrow_phase(s1, 1, 0, reps) if len(s1) else 0.0
-    n = len(p1) + len(s1)
-    return n / (tp + ts), {"rays": n, "stride": step, "seconds": reps * (tp + ts), "reps": reps}
+    total = sum(model.time_narrow_phase(r, mode, 0, reps) for r, mode in sets if len(r))
+    return n / total, {"rays": n, "seconds": reps * total, "reps": reps}
+
+
+def pairs_fraction(model, rays: np.ndarray) -> float:
+    """Fraction of rays that form a pair (CPU MLP rows) on a subsample."""
+    sub = rays[:: max(1, len(rays) // 16384)]
+    info = model.trace(sub)["info"]
+    return float(np.mean((info >> 9) & 1 == 1))
+
+
+def sample_parity(gpu_hits: np.ndarray, ref_hits: np.ndarray) -> dict:
+    """Parity of a GPU result sample against the CPU reference on the same
+    rays (SURVEY App. B gates): pair flags bit-exact, visibility / material
+    agreement, and for rays both call occluded the t, normal and albedo
+    deviations."""
+    f_g, f_r = gpu_hits["flags_material"], ref_hits["flags_material"]
+    pair = (f_r & 1) == 1
+    occ_g, occ_r = (f_g & 2) != 0, (f_r & 2) != 0
+    both = pair & occ_g & occ_r
+    mat_g, mat_r = f_g >> 8, f_r >> 8
+    out = {"rays": int(len(f_r)), "pairs": int(pair.sum()),
+           "pair_flags_equal": bool(np.array_equal(f_g & 1, f_r & 1)),
+           "visibility_agree": float(np.mean(occ_g[pair] == occ_r[pair])) if pair.any() else 1.0,
+           "material_agree": float(np.mean(mat_g[pair] == mat_r[pair])) if pair.any() else 1.0,
+           "both_occluded": int(both.sum())}
+    if both.any():
+        ng, nr = gpu_hits["normal"][both].astype(np.float64), ref_hits["normal"][both].astype(np.float64)
+        lg, lr = np.linalg.norm(ng, axis=1), np.linalg.norm(nr, axis=1)
+        ok = (lg > 0) & (lr > 0)
+        cosv = np.clip(np.sum(ng[ok] * nr[ok], axis=1) / (lg[ok] * lr[ok]), -1, 1)
+        out.update({"max_dt_world": float(np.max(np.abs(gpu_hits["t_world"][both] - ref_hits["t_world"][both]))),
+                    "max_normal_deg": float(np.degrees(np.max(np.arccos(cosv)))) if ok.any() else 0.0,
+                    "max_dalbedo": float(np.max(np.abs(gpu_hits["albedo"][both] - ref_hits["albedo"][both])))})
+    return out
 
 
 # ---------------------------------------------------------------- reference
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference's CPU algorithm (oracle port of
-    run_narrow_phase + infer_batch, -O3 -march=native, all host threads) on a
-    bounded sample of this arm's workload."""
+    """--impl reference: the reference's CPU algorithm (run_narrow_phase +
+    infer_batch, -O3 -march=native, all host threads) on a bounded sample of
+    this arm's workload — for C5 and C2 exactly the rays our arm's
+    cpu_baseline times (same indices / the same shadow set). Under torchrun
+    only rank 0 runs; the other ranks exit without work."""
     if rank != 0:
         return 0
     O = cpu_oracle(True)
-    from paper_2504_21627_b200 import workloads as W
     model = O.OracleModel.load(MODEL_PATH, fast=True)
-    primary = build_rays(args.workload, 0, model.aabb)
-    mode0 = 0
     cores = int(O.lib(True).oracle_hardware_concurrency())
-    # bounded sample sized for ~2 s of CPU work per step
-    probe = primary[:: max(1, len(primary) // 8192)]
-    t0 = time.perf_counter()
-    model.narrow_phase(probe, mode0, 0)
-    rate = len(probe) / max(time.perf_counter() - t0, 1e-6)
-    stride = max(1, int(len(primary) / max(rate * 2.0, 1.0)))
-    prim = primary[::stride]
-    hits = model.narrow_phase(prim, mode0, 0)
-    shadow = W.shadow_rays(prim, hits, model.aabb)[0] if args.workload == "c2" else prim[:0]
+    box = model.aabb
+    if args.workload == "c5":
+        _, rays = c5_sample(box, args.rays or C5_RAYS)
+        sets = [(rays, 0)]
+        sample = (f"every {C5_CPU_STRIDE}th ray of the C5 frame ({len(rays)} rays, the same indices the "
+                  f"GPU arm's cpu_baseline times)")
+    elif args.workload == "c2":
+        prim = build_rays("c2", 0, box)
+        shadow = c2_shadow_set(prim, box)
+        sets = [(prim, 0), (shadow, 1)]
+        sample = (f"the whole C2 frame: {len(prim)} primary rays + {len(shadow)} shadow rays "
+                  f"(the shadow set every arm answers)")
+    else:
+        prim = build_rays(args.workload, 0, box)
+        stride = max(1, len(prim) // (1 << 21))
+        sets = [(prim[::stride], 0)]
+        sample = f"every {stride}th ray of the {args.workload.upper()} set ({len(sets[0][0])} rays)"
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        model.narrow_phase(prim, mode0, 0)
-        if len(shadow):
-            model.narrow_phase(shadow, 1, 0)
+        for r, mode in sets:
+            model.narrow_phase(r, mode, 0)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
-    n = len(prim) + len(shadow)
+    n = sum(len(r) for r, _ in sets)
     total = sum(times)
     value = n * len(times) / total
-    # MLP rows per ray on a small subsample (oracle trace: rays with >= 1 point)
-    both = np.concatenate([prim, shadow]) if len(shadow) else prim
-    sub = both[:: max(1, len(both) // 8192)]
-    info = model.trace(sub)["info"]
-    rows = float(np.mean(((info >> 9) & 1 == 1) & ((info & 255) > 0)))
-    ref_detail = cpu_detail(value, cores, rows, model.hidden, model.input_width, 8 + model.n_mat)
-    sample = (f"every {stride}th ray of the {args.workload.upper()} primary set "
-              f"({len(prim)} rays) + {len(shadow)} shadow rays from the oracle's own hits")
+    pf = pairs_fraction(model, np.concatenate([r for r, _ in sets]))
+    ref_detail = cpu_detail(value, cores, pf, model.hidden, model.input_width, 8 + model.n_mat)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload], "rays_per_step": n,
                    "parallelism": "host threads (parallel_slices)"},
         "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -577,236 +626,463 @@ def run_render(args, rank, world, dev, gpu, max_over_ranks):
 
 # --------------------------------------------------------------------- ours
 
-def main():
-    args = parse_args()
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return run_reference(args, rank, world)
+class Ctx:
+    """Rank / device / collective plumbing shared by the workload runners."""
 
-    import torch
-    import torch.distributed as dist
-    from paper_2504_21627_b200 import lsnif, workloads as W
+    def __init__(self, args):
+        import torch
+        import torch.distributed as dist
+        self.args = args
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.gloo = args.dist_backend == "gloo"
+        self.gpu = 0 if self.gloo else self.local_rank
+        torch.cuda.set_device(self.gpu)
+        self.dev = torch.device("cuda", self.gpu)
+        if self.world > 1:
+            if self.gloo:
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=self.dev)
+        self.coll_dev = torch.device("cpu") if self.gloo else self.dev
 
-    gloo = args.dist_backend == "gloo"
-    gpu = 0 if gloo else local_rank
-    torch.cuda.set_device(gpu)
-    dev = torch.device("cuda", gpu)
-    if world > 1:
-        if gloo:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
-    coll_dev = torch.device("cpu") if gloo else dev
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
 
-    def max_over_ranks(x: float) -> float:
-        if world == 1:
+    def max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([x], dtype=torch.float64, device=self.coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    if args.workload in ("c4", "render"):
-        (run_c4 if args.workload == "c4" else run_render)(args, rank, world, dev, gpu, max_over_ranks)
-        if world > 1:
+    def sum_over_ranks(self, xs):
+        if self.world == 1:
+            return list(xs)
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor(list(xs), dtype=torch.float64, device=self.coll_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return [float(v) for v in t.tolist()]
+
+    def close(self):
+        if self.world > 1:
+            import torch.distributed as dist
             dist.barrier()
             dist.destroy_process_group()
-        return 0
 
-    model = lsnif.GpuModel(MODEL_PATH, gpu)
-    box = model.aabb
-    strong = args.workload == "c5"
-    primary = build_rays(args.workload, rank, box, world)
-    d_primary = lsnif.rays_to_tensor(primary, dev)
-    d_hits_p = torch.empty((len(primary), 8), dtype=torch.int32, device=dev)
-    mode_p = lsnif.CLOSEST
-    model.query(d_primary, mode_p, out=d_hits_p)
-    stats_p = model.last_stats()
-    hits_p = lsnif.hits_to_numpy(d_hits_p)
-    if args.workload == "c2":
-        shadow, _ = W.shadow_rays(primary, hits_p, box)
-    else:
-        shadow = primary[:0]
-    d_shadow = lsnif.rays_to_tensor(shadow, dev) if len(shadow) else None
-    d_hits_s = torch.empty((max(len(shadow), 1), 8), dtype=torch.int32, device=dev)
-    stats_s = {"rays": 0, "pairs": 0, "mlp_rows": 0, "points": 0, "volume_points": 0}
-    if len(shadow):
-        model.query(d_shadow, lsnif.ANY, out=d_hits_s)
-        stats_s = model.last_stats()
-    n_step = len(primary) + len(shadow)
-    gathered = {}
-    gather_out, gather_sizes = None, None
-    if strong and world > 1:  # C5: every rank's band size is known from the partition
-        from paper_2504_21627_b200.dist import ray_range
-        gather_sizes = [ray_range(3840 * 2160 * 16, world, r)[1] - ray_range(3840 * 2160 * 16, world, r)[0]
-                        for r in range(world)]
-        if rank == 0:
-            gather_out = torch.empty((sum(gather_sizes), 8), dtype=torch.int32,
-                                     device=dev if not gloo else "cpu")
 
-    def step():
-        model.query(d_primary, mode_p, out=d_hits_p)
-        if d_shadow is not None:
-            model.query(d_shadow, lsnif.ANY, out=d_hits_s)
-        if strong and world > 1:  # the one collective: result gather to rank 0 (preallocated)
-            from paper_2504_21627_b200.dist import gather_to_rank0
-            gathered["hits"] = gather_to_rank0(d_hits_p if not gloo else d_hits_p.cpu(),
-                                               out=gather_out, sizes=gather_sizes)
-
-    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
-    for _ in range(args.warmup):
+def timed_steps(ctx, step, steps: int, warmup: int, flush, model=None):
+    """W untimed steps, then K steps each bracketed by CUDA events on the
+    launching stream (L2 flushed outside the events), barrier + synchronize
+    on both sides, clocks sampled during the timed region. Returns
+    (max-over-ranks device ms of the K steps, clock summary, launches)."""
+    import torch
+    for _ in range(warmup):
         step()
     torch.cuda.synchronize()
-
-    clocks = ClockSampler(local_rank)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    model.profile_read(reset=True)          # launch counts of the timed region
+    if model is not None:
+        model.profile_read(reset=True, stream="all")
+    clocks = ClockSampler(ctx.gpu)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     clocks.start()
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
     torch.cuda.synchronize()
-    for k in range(args.steps):
-        flush.zero_()                       # L2 flush, outside the timed events
+    for k in range(steps):
+        flush.zero_()
         ev[k][0].record()
         step()
         ev[k][1].record()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
     clocks.stop()
-    timed = model.profile_read(reset=True)
-    # per-kernel breakdown in a separate, identical pass: the library's
-    # per-kernel CUDA events are not part of the timed steps above
+    launches = model.profile_read(reset=True, stream="all")["launches"] if model is not None else 0
+    elapsed = ctx.max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
+    return elapsed, clocks.summary(), launches
+
+
+def kernel_breakdown(model, step, steps: int, flush):
+    """Per-kernel device time of the same step in a separate profiled pass
+    (the library's per-launch CUDA events are not part of the timed steps)."""
+    import torch
+    model.profile_read(reset=True, stream="all")
     model.profile_enable(True)
-    for k in range(args.steps):
+    for _ in range(steps):
         flush.zero_()
         step()
     torch.cuda.synchronize()
     model.profile_enable(False)
-    prof = model.profile_read(reset=True)
-    prof["launches"] = timed["launches"]
-    elapsed_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
-    # weak scaling: every rank answers its own frame; strong (C5): one frame split
-    total_rays = n_step if strong and world == 1 else world * n_step
-    if strong:
-        total_rays = 3840 * 2160 * 16
-    value = total_rays * args.steps / (elapsed_ms / 1e3)
+    return model.profile_read(reset=True, stream="all")
 
-    # ---- e2e: same step through the host C-ABI entry (pinned buffers)
+
+def kernel_roofline(model, prof, steps: int, n_rays: int, rows: int, pts: int, vol: int, result_bytes: int,
+                    peaks: dict, tag: str) -> tuple[dict, dict, float]:
+    """`roofline` of the dominant kernel (SURVEY §8(d) per-unit figures x the
+    units one launch processes ÷ its average launch time) + the kernels map."""
+    tr_ms = prof["trace_ms"] / steps
+    ml_ms = prof["mlp_ms"] / steps
+    hid = model.info.hidden
+    mlp_flops = 2 * rows * (model.input_width * hid + hid * hid + hid * (8 + model.info.n_mat))
+    # trace_encode_kernel: rays in (32 B), results of rays without MLP rows,
+    # 48 B of hash-table entries per boundary / volume point
+    trace_bytes = 32 * n_rays + result_bytes * (n_rays - rows) + 48 * pts + 48 * vol
+    traffic = load_json(f"traffic_{tag}.json")  # ncu DRAM bytes per launch (profiles/)
+    if tr_ms >= ml_ms:
+        launches = max(1, prof["trace_launches"] // steps)
+        ach = trace_bytes / (tr_ms / 1e3) / 1e9
+        roof = {"kernel": "trace_encode_kernel", "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": ach / peaks["hbm_gbs"], "traffic": traffic.get("trace_encode_kernel"),
+                "algorithmic_bytes_per_launch": trace_bytes / launches, "launches_per_step": launches,
+                "peak_source": peaks["source"]}
+    else:
+        launches = max(1, prof["mlp_launches"] // steps)
+        ach = mlp_flops / (ml_ms / 1e3) / 1e12
+        pk = peaks.get("bf16_tflops", peaks.get("bf16_tflops_sustained", 1400.0))
+        roof = {"kernel": "mlp_tc_kernel", "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+                "frac": ach / pk, "traffic": traffic.get("mlp_tc_kernel"), "peak_source": peaks["source"]}
+    kernels = {"trace_encode_kernel": {"ms_per_step": tr_ms, "launches": prof["trace_launches"],
+                                       "GBps_algorithmic": trace_bytes / (tr_ms / 1e3) / 1e9 if tr_ms else None},
+               "mlp_tc_kernel": {"ms_per_step": ml_ms, "launches": prof["mlp_launches"],
+                                 "tflops": mlp_flops / (ml_ms / 1e3) / 1e12 if ml_ms > 0 else None,
+                                 "frac_of_burst_peak": (mlp_flops / (ml_ms / 1e3) / 1e12) /
+                                 peaks.get("bf16_tflops", 1614.9) if ml_ms > 0 else None}}
+    return roof, kernels, mlp_flops
+
+
+def run_c5(args, ctx) -> None:
+    """C5: one 132.7M-ray frame split into row bands (one per rank); see the
+    module docstring."""
+    import torch
+    import torch.distributed as dist
+    from paper_2504_21627_b200 import lsnif, workloads as W
+    from paper_2504_21627_b200.dist import gather_piece_to_rank0, piece_range, ray_range
+    rank, world = ctx.rank, ctx.world
+    total = args.rays or C5_RAYS
+    bands = [ray_range(total, world, r) for r in range(world)]
+    sizes = [e - s for s, e in bands]
+    s0, band = bands[rank][0], sizes[rank]
+    model = lsnif.GpuModel(MODEL_PATH, ctx.gpu)
+    box = model.aabb
+    # the rank's rays, regenerated from the index-addressable generator into
+    # pinned host memory (the e2e input) and copied once to the device
+    pin_rays = torch.empty((band, 8), dtype=torch.float32, pin_memory=True)
+    W.incoherent_rays_into(pin_rays.numpy(), box, C5_SEED, s0)
+    d_rays = pin_rays.to(ctx.dev)
+    pieces = C5_PIECES if world > 1 else 1
+    d_frame = torch.empty((total, 4), dtype=torch.int32, device=ctx.dev) if rank == 0 else None
+    local = d_frame[:band] if rank == 0 else torch.empty((band, 4), dtype=torch.int32, device=ctx.dev)
+    comm = torch.cuda.Stream(ctx.dev) if world > 1 and not ctx.gloo else None
+    cpu_frame = torch.empty((total, 4), dtype=torch.int32) if ctx.gloo and rank == 0 else None
+    pev = [torch.cuda.Event() for _ in range(pieces)]
+
+    def step():
+        works = []
+        for k in range(pieces):
+            ps, pe = piece_range(band, pieces, k)
+            model.query_wire(d_rays[ps:pe], lsnif.CLOSEST, out=local[ps:pe])
+            if world == 1:
+                continue
+            if ctx.gloo:  # test mode: every rank on cuda:0, the gather through host tensors
+                piece = local[ps:pe].cpu()
+                if rank == 0:
+                    cpu_frame[ps:pe].copy_(piece)
+                for w in gather_piece_to_rank0(piece, k, pieces, sizes, out=cpu_frame):
+                    w.wait()
+            else:  # piece k goes to rank 0 on the comm stream while piece k + 1 computes
+                pev[k].record()
+                with torch.cuda.stream(comm):
+                    comm.wait_event(pev[k])
+                    works += gather_piece_to_rank0(local[ps:pe], k, pieces, sizes, out=d_frame)
+        if world > 1 and not ctx.gloo:
+            with torch.cuda.stream(comm):
+                for w in works:
+                    w.wait()
+            torch.cuda.current_stream().wait_stream(comm)
+        if ctx.gloo and rank == 0:
+            d_frame.copy_(cpu_frame)
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=ctx.dev)
+    step()  # warm (NCCL connection setup, staging, launch configuration)
+    torch.cuda.synchronize()
+    # per-band query statistics (pairs, MLP rows, points) for the rooflines
+    st = np.zeros(4)
+    for k in range(pieces):
+        ps, pe = piece_range(band, pieces, k)
+        model.query_wire(d_rays[ps:pe], lsnif.CLOSEST, out=local[ps:pe])
+        s = model.last_stats()
+        st += [s["pairs"], s["mlp_rows"], s["points"], s["volume_points"]]
+    pairs, rows, pts, vol = [int(v) for v in st]
+    elapsed_ms, clocks, launches = timed_steps(ctx, step, args.steps, max(args.warmup - 1, 0), flush, model)
+    prof = kernel_breakdown(model, step, args.steps, flush)
+    value = total * args.steps / (elapsed_ms / 1e3)
+    tot_stats = ctx.sum_over_ranks([pairs, rows, pts, vol])
+
+    # ---- e2e: lsnif_query_host_wire from pinned host rays; every rank's band
+    # lands in one full-frame host buffer (shared memory on this node, pinned)
+    lib = lsnif.load_library()
+    host_frame, host_note, shm_path = None, "", None
+    if world == 1:
+        host_frame = torch.empty((total, 4), dtype=torch.int32, pin_memory=True)
+        host_note = "pinned host frame"
+    else:
+        tag = os.environ.get("MASTER_PORT", "0")
+        shm_path = f"/dev/shm/lsnif_c5_{tag}.frame"
+        need = total * 16
+        ok = 1.0
+        try:
+            sv = os.statvfs("/dev/shm")
+            ok = 1.0 if sv.f_bavail * sv.f_frsize > need * 1.05 else 0.0
+        except OSError:
+            ok = 0.0
+        ok = -ctx.max_over_ranks(-ok)  # min over ranks
+        if ok > 0:
+            if rank == 0:
+                with open(shm_path, "wb") as f:
+                    f.truncate(need)
+            ctx.barrier()
+            mm = np.memmap(shm_path, dtype=np.int32, mode="r+", shape=(total, 4))
+            host_frame = torch.from_numpy(np.asarray(mm))
+            rc = torch._C._cudart.cudaHostRegister(host_frame.data_ptr(), need, 0)
+            if int(rc) != 0:
+                raise RuntimeError(f"cudaHostRegister of the shared host frame failed ({rc})")
+            ctx.barrier()
+            if rank == 0:
+                os.unlink(shm_path)
+            host_note = "one full-frame host buffer shared by the ranks (/dev/shm, cudaHostRegister-ed)"
+        else:
+            host_frame = torch.empty((band, 4), dtype=torch.int32, pin_memory=True)
+            host_note = "per-rank pinned band buffers (/dev/shm too small for a shared frame)"
+    off = s0 if host_frame.shape[0] == total else 0
+
+    def e2e_step():
+        lsnif._check(lib.lsnif_query_host_wire(model.h, pin_rays.data_ptr(), band, lsnif.CLOSEST,
+                                               host_frame.data_ptr() + 16 * off, None))
+
+    e2e_step()
+    e2e_steps = max(3, min(args.steps, 6))
+    per_step = []
+    for _ in range(e2e_steps):
+        ctx.barrier()
+        t0 = time.perf_counter()
+        e2e_step()
+        ctx.barrier()  # the frame is complete when every band has landed
+        per_step.append(time.perf_counter() - t0)
+    e2e_s = ctx.max_over_ranks(float(np.median(per_step)))
+    e2e_value = total / e2e_s
+    # bit-identical frames: host API path vs the device path (+ NCCL gather)
+    same = True
+    if rank == 0:
+        d_host = d_frame.cpu()
+        same = bool(torch.equal(host_frame[:band], d_host[:band])) if host_frame.shape[0] != total else \
+            bool(torch.equal(host_frame, d_host))
+        assert same, "host-API frame differs from the device frame"
+        if args.dump:
+            np.save(args.dump, d_host.numpy())
+    ctx.barrier()
+
+    if rank == 0:
+        peaks = load_peaks()
+        roof, kernels, mlp_flops = kernel_roofline(model, prof, args.steps, band, rows, pts, vol, 16, peaks, "c5")
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 traversal/encode + f16xf16->f32 tcgen05 MLP", "data": "synthetic",
+            "config": {"workload": WORKLOADS["c5"] if total == C5_RAYS else
+                       WORKLOADS["c5"] + f" [TEST SIZE: {total} rays]",
+                       "rays_per_step": total, "rays_per_gpu": sizes, "pieces_per_band": pieces,
+                       "result_record_bytes": 16,
+                       "l2": "inputs (4.25 GB of rays) far larger than L2; also flushed between timed steps "
+                             "(256 MiB write outside the events)",
+                       "parallelism": f"dp{world} (row bands of one frame" +
+                                      (", pieces gathered point-to-point to rank 0 over NCCL, overlapped "
+                                       "with compute)" if world > 1 else ")")},
+            "workload_stats": {"frac_hit_aabb": tot_stats[0] / total, "frac_ge1_point": tot_stats[1] / total,
+                               "mean_points": tot_stats[2] / total, "volume_points": int(tot_stats[3])},
+            "roofline": roof,
+            "path_roofline": path_roofline(value / world, band, rows, pts, vol, mlp_flops, peaks, 16),
+            "kernels": kernels,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 32 * total,
+                    "d2h_bytes_per_step": 16 * total, "steps": e2e_steps,
+                    "timing": "median step (host clock, barriers on both sides), max over ranks",
+                    "step_ms_min_median_max": [1e3 * min(per_step), 1e3 * float(np.median(per_step)),
+                                               1e3 * max(per_step)],
+                    "api": "lsnif_query_host_wire per rank (pinned host rays -> chunked H2D / query / D2H of "
+                           "16 B wire results) into " + host_note,
+                    "bit_identical_to_device_frame": same},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        line.update(aux_rooflines("c5", band / (kernels["trace_encode_kernel"]["ms_per_step"] / 1e3)
+                                  if kernels["trace_encode_kernel"]["ms_per_step"] else 0.0,
+                                  clocks.get("sm_mhz"), pts / band, vol / band))
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                O = cpu_oracle(True)
+                om = O.OracleModel.load(MODEL_PATH, fast=True)
+                idx, srays = c5_sample(box, total)
+                rate, info = time_cpu_sets(om, [(srays, 0)], args.cpu_seconds)
+                cores = int(O.lib(True).oracle_hardware_concurrency())
+                line["cpu_baseline"] = {
+                    "value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                    "sample": f"every {C5_CPU_STRIDE}th ray of the C5 frame ({info['rays']} rays, the "
+                              f"reference arm's rays), best of {info['reps']} passes (~{info['seconds']:.1f} s "
+                              f"of CPU work)"}
+                line["cpu_baseline"].update(cpu_detail(rate, cores, pairs_fraction(om, srays), model.info.hidden,
+                                                       model.input_width, 8 + model.info.n_mat))
+                # the sample doubles as a parity spot check of the timed frame
+                gpu = lsnif.wire_to_hits(d_frame.cpu().numpy()[idx.astype(np.int64)])
+                line["sample_parity"] = sample_parity(gpu, om.narrow_phase(srays, 0, 0))
+            except Exception as e:  # reported, never silently substituted
+                line["cpu_baseline"] = {"value": None, "error": str(e)}
+        print(json.dumps(line), flush=True)
+    if host_frame is not None and world > 1 and host_frame.shape[0] == total:
+        torch._C._cudart.cudaHostUnregister(host_frame.data_ptr())
+
+
+def run_single(args, ctx) -> None:
+    """C1 / C2 / C3: one frame per rank (weak scaling, no data-path collective)."""
+    import torch
+    from paper_2504_21627_b200 import lsnif
+    rank, world = ctx.rank, ctx.world
+    model = lsnif.GpuModel(MODEL_PATH, ctx.gpu)
+    box = model.aabb
+    primary = build_rays(args.workload, rank, box, world)
+    shadow = c2_shadow_set(primary, box) if args.workload == "c2" else primary[:0]
+    d_primary = lsnif.rays_to_tensor(primary, ctx.dev)
+    d_hits_p = torch.empty((len(primary), 8), dtype=torch.int32, device=ctx.dev)
+    d_shadow = lsnif.rays_to_tensor(shadow, ctx.dev) if len(shadow) else None
+    d_hits_s = torch.empty((len(shadow), 8), dtype=torch.int32, device=ctx.dev)
+    st = np.zeros(4)
+    for rays, hits, mode in ((d_primary, d_hits_p, lsnif.CLOSEST), (d_shadow, d_hits_s, lsnif.ANY)):
+        if rays is not None:
+            model.query(rays, mode, out=hits)
+            s = model.last_stats()
+            st += [s["pairs"], s["mlp_rows"], s["points"], s["volume_points"]]
+    pairs, rows, pts, vol = [int(v) for v in st]
+    n_step = len(primary) + len(shadow)
+
+    def step():
+        model.query(d_primary, lsnif.CLOSEST, out=d_hits_p)
+        if d_shadow is not None:
+            model.query(d_shadow, lsnif.ANY, out=d_hits_s)
+
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=ctx.dev)
+    elapsed_ms, clocks, launches = timed_steps(ctx, step, args.steps, args.warmup, flush, model)
+    prof = kernel_breakdown(model, step, args.steps, flush)
+    value = world * n_step * args.steps / (elapsed_ms / 1e3)
+
+    # ---- e2e: the same step through the host C-ABI entry (pinned buffers,
+    # 16 B wire results)
     pin_p = torch.from_numpy(primary.view(np.float32).reshape(-1, 8).copy()).pin_memory()
-    hp = torch.empty((len(primary), 8), dtype=torch.int32).pin_memory()
-    pin_s = torch.from_numpy(shadow.view(np.float32).reshape(-1, 8).copy()).pin_memory() \
-        if len(shadow) else None
-    hs = torch.empty((max(len(shadow), 1), 8), dtype=torch.int32).pin_memory()
+    hp = torch.empty((len(primary), 4), dtype=torch.int32).pin_memory()
+    pin_s = torch.from_numpy(shadow.view(np.float32).reshape(-1, 8).copy()).pin_memory() if len(shadow) else None
+    hs = torch.empty((max(len(shadow), 1), 4), dtype=torch.int32).pin_memory()
     lib = lsnif.load_library()
 
     def e2e_step():
-        lsnif._check(lib.lsnif_query_host(model.h, pin_p.data_ptr(), len(primary), mode_p,
-                                          hp.data_ptr(), None))
+        lsnif._check(lib.lsnif_query_host_wire(model.h, pin_p.data_ptr(), len(primary), lsnif.CLOSEST,
+                                               hp.data_ptr(), None))
         if pin_s is not None:
-            lsnif._check(lib.lsnif_query_host(model.h, pin_s.data_ptr(), len(shadow), lsnif.ANY,
-                                              hs.data_ptr(), None))
+            lsnif._check(lib.lsnif_query_host_wire(model.h, pin_s.data_ptr(), len(shadow), lsnif.ANY,
+                                                   hs.data_ptr(), None))
 
     e2e_step()
     e2e_steps = max(5, min(args.steps, 15))
-    if world > 1:
-        dist.barrier()
+    ctx.barrier()
     torch.cuda.synchronize()
-    # each step timed on the host clock (the call is synchronous: H2D, query,
-    # D2H complete on return); the median step of each rank, max over ranks,
-    # so one host hiccup does not decide the figure
     per_step = []
     for _ in range(e2e_steps):
         t0 = time.perf_counter()
         e2e_step()
         per_step.append(time.perf_counter() - t0)
-    e2e_s = max_over_ranks(float(np.median(per_step)))
-    e2e_value = total_rays / e2e_s
-    assert np.array_equal(hp.numpy(), d_hits_p.cpu().numpy()), "host/device results differ"
+    e2e_s = ctx.max_over_ranks(float(np.median(per_step)))
+    e2e_value = world * n_step / e2e_s
+    # wire results carry the parity record's flags, material and t bit for bit
+    dp = lsnif.hits_to_numpy(d_hits_p)
+    wp = hp.numpy().view(lsnif.WIRE_DTYPE).reshape(-1)
+    assert np.array_equal(wp["flags_material"], dp["flags_material"]) and \
+        np.array_equal(wp["t_world"].view(np.uint32), dp["t_world"].view(np.uint32)), "wire/device results differ"
 
     if rank == 0:
         peaks = load_peaks()
-        tr_ms = prof["trace_ms"] / args.steps
-        ml_ms = prof["mlp_ms"] / args.steps
-        rows = stats_p["mlp_rows"] + stats_s["mlp_rows"]
-        pts = stats_p["points"] + stats_s["points"]
-        vol = stats_p["volume_points"] + stats_s["volume_points"]
-        # algorithmic bytes of trace_encode_kernel per step (SURVEY §8(d) B_ray,
-        # minus the 32 B results the MLP kernel writes for MLP rows)
-        trace_bytes = 32 * n_step + 32 * (n_step - rows) + 48 * pts + 48 * vol
-        mlp_flops = 2 * rows * (model.input_width * model.info.hidden + model.info.hidden ** 2 +
-                                model.info.hidden * (8 + model.info.n_mat))
-        traffic = load_traffic(args.workload)
-        if tr_ms >= ml_ms:
-            launches = max(1, prof["trace_launches"] // args.steps)
-            ach = trace_bytes / (tr_ms / 1e3) / 1e9
-            roof = {"kernel": "trace_encode_kernel", "bound": "hbm", "achieved": ach,
-                    "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach / peaks["hbm_gbs"],
-                    "traffic": traffic.get("trace_encode_kernel"),
-                    "algorithmic_bytes_per_launch": trace_bytes / launches,
-                    "peak_source": peaks["source"]}
-        else:
-            launches = max(1, prof["mlp_launches"] // args.steps)
-            ach = mlp_flops / (ml_ms / 1e3) / 1e12
-            pk = peaks.get("bf16_tflops_sustained", 1400.0)
-            roof = {"kernel": "mlp_tc_kernel", "bound": "tensor", "achieved": ach, "peak": pk,
-                    "unit": "TFLOP/s", "frac": ach / pk, "traffic": traffic.get("mlp_tc_kernel"),
-                    "peak_source": peaks["source"]}
+        roof, kernels, mlp_flops = kernel_roofline(model, prof, args.steps, n_step, rows, pts, vol, 32, peaks,
+                                                   args.workload)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
             "dtype": "f32 traversal/encode + f16xf16->f32 tcgen05 MLP", "data": "synthetic",
             "config": {"workload": WORKLOADS[args.workload], "rays_per_step_per_gpu": n_step,
                        "primary_rays": len(primary), "shadow_rays": len(shadow),
                        "l2": "flushed between timed steps (256 MiB write outside the events)",
-                       "parallelism": (f"dp{world} (row bands of one frame + NCCL result gather)"
-                                       if strong else
-                                       f"dp{world} (one frame per GPU, no data-path collective)")},
-            "workload_stats": {
-                "frac_hit_aabb": (stats_p["pairs"] + stats_s["pairs"]) / n_step,
-                "frac_ge1_point": rows / n_step, "mean_points": pts / n_step,
-                "volume_points": vol},
+                       "parallelism": f"dp{world} (one frame per GPU, no data-path collective)"},
+            "workload_stats": {"frac_hit_aabb": pairs / n_step, "frac_ge1_point": rows / n_step,
+                               "mean_points": pts / n_step, "volume_points": vol},
             "roofline": roof,
-            "path_roofline": path_roofline(value / world, n_step, rows, pts, vol,
-                                           mlp_flops, peaks),
-            "kernels": {"trace_encode_kernel": {"ms_per_step": tr_ms,
-                                                "launches": prof["trace_launches"]},
-                        "mlp_tc_kernel": {"ms_per_step": ml_ms,
-                                          "launches": prof["mlp_launches"],
-                                          "tflops": mlp_flops / (ml_ms / 1e3) / 1e12
-                                          if ml_ms > 0 else None}},
+            "path_roofline": path_roofline(value / world, n_step, rows, pts, vol, mlp_flops, peaks, 32),
+            "kernels": kernels,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 32 * n_step,
-                    "d2h_bytes_per_step": 32 * n_step, "steps": e2e_steps, "timing": "median step, max over ranks",
-                    "step_ms_min_median_max": [1e3 * min(per_step), 1e3 * float(np.median(per_step)), 1e3 * max(per_step)],
-                    "api": "lsnif_query_host (pinned host rays/hits, chunked H2D/query/D2H)"},
-            "gpu_launches": prof["launches"],
-            "clocks": clocks.summary(),
+                    "d2h_bytes_per_step": 16 * n_step, "steps": e2e_steps,
+                    "timing": "median step, max over ranks",
+                    "step_ms_min_median_max": [1e3 * min(per_step), 1e3 * float(np.median(per_step)),
+                                               1e3 * max(per_step)],
+                    "api": "lsnif_query_host_wire (pinned host rays -> 16 B wire results, chunked H2D/query/D2H)"},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
         }
-        line.update(aux_rooflines(args.workload, n_step / (tr_ms / 1e3) if tr_ms > 0 else 0.0,
-                                  line["clocks"].get("sm_mhz"), pts / n_step, vol / n_step))
+        line.update(aux_rooflines(args.workload, n_step / (kernels["trace_encode_kernel"]["ms_per_step"] / 1e3)
+                                  if kernels["trace_encode_kernel"]["ms_per_step"] else 0.0,
+                                  clocks.get("sm_mhz"), pts / n_step, vol / n_step))
         if world == 1 and not args.no_cpu_baseline:
             try:
                 O = cpu_oracle(True)
                 om = O.OracleModel.load(MODEL_PATH, fast=True)
-                rate, info = time_cpu(O, om, primary, shadow, args.cpu_seconds)
+                if args.workload == "c3":
+                    sets = [(primary[::8], 0)]
+                    smp = f"every 8th C3 ray ({len(sets[0][0])} rays)"
+                else:
+                    sets = [(primary, 0), (shadow, 1)]
+                    smp = f"the whole frame: {len(primary)} primary + {len(shadow)} shadow rays"
+                rate, info = time_cpu_sets(om, sets, args.cpu_seconds)
                 cores = int(O.lib(True).oracle_hardware_concurrency())
-                line["cpu_baseline"] = {
-                    "value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                    "sample": f"every {info['stride']}th primary and shadow ray of this "
-                              f"workload ({info['rays']} rays), best of {info['reps']} passes "
-                              f"(~{info['seconds']:.1f} s of CPU work)"}
-                line["cpu_baseline"].update(cpu_detail(rate, cores, rows / n_step, model.info.hidden,
-                                                       model.input_width, 8 + model.info.n_mat))
-            except Exception as e:  # reported, never silently substituted
+                line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                                        "sample": f"{smp}, best of {info['reps']} passes "
+                                                  f"(~{info['seconds']:.1f} s of CPU work)"}
+                line["cpu_baseline"].update(cpu_detail(rate, cores,
+                                                       pairs_fraction(om, np.concatenate([r for r, _ in sets])),
+                                                       model.info.hidden, model.input_width, 8 + model.info.n_mat))
+            except Exception as e:
                 line["cpu_baseline"] = {"value": None, "error": str(e)}
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.barrier()
-        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        return relaunch_under_torchrun(args)
+    if world_env is not None and int(world_env) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}", file=sys.stderr)
+        return 2
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(world_env or "1")
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    ctx = Ctx(args)
+    if args.workload == "c5":
+        run_c5(args, ctx)
+    elif args.workload in ("c4", "render"):
+        (run_c4 if args.workload == "c4" else run_render)(args, ctx.rank, ctx.world, ctx.dev, ctx.gpu,
+                                                          ctx.max_over_ranks)
+    else:
+        run_single(args, ctx)
+    ctx.close()
     return 0
 
 

@@ -69,6 +69,24 @@ typedef struct lsnif_hit {
 #define LSNIF_HIT_ACCEPTED 4u
 #define LSNIF_HIT_MATERIAL_SHIFT 8
 
+/* Packed 16 B "wire" form of lsnif_hit, SURVEY.md §2.1 (parity layout fp32
+ * fields, wire layout packed): for results that cross PCIe or NVLink.
+ *   flags_material, t_world   bit-identical to the lsnif_hit fields;
+ *   normal_oct    the unit normal, octahedral map, 2 x snorm16 (u low,
+ *                 v high); angular error < 0.01 degree;
+ *   albedo_unorm  3 x unorm10 (r bits 0-9, g 10-19, b 20-29), error
+ *                 <= 0.5/1023; bit 30 set when the normal is zero (NeuralHit's
+ *                 zero-length normal, renderer.cpp:216-219).
+ * lsnif_hits_from_wire expands it back to lsnif_hit on the host. */
+typedef struct lsnif_hit_wire {
+  uint32_t flags_material;
+  float t_world;
+  uint32_t normal_oct;
+  uint32_t albedo_unorm;
+} lsnif_hit_wire;
+
+#define LSNIF_WIRE_ZERO_NORMAL 0x40000000u
+
 /* lsnif::Material (geometry.hpp:56-60), as stored in the model file. */
 typedef struct lsnif_material {
   float albedo[3];
@@ -158,6 +176,15 @@ lsnif_status lsnif_query_any(lsnif_model model, const lsnif_ray* d_rays, const l
  * overlapped on internal streams. Synchronous. */
 lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_t n, int mode,
                               lsnif_hit* h_hits, void* stream);
+
+/* lsnif_query / lsnif_query_host writing the packed 16 B wire records
+ * (half the result bytes of lsnif_hit; same flags, material and t_world). */
+lsnif_status lsnif_query_wire(lsnif_model model, const lsnif_ray* d_rays, int64_t n, int mode,
+                              lsnif_hit_wire* d_hits, void* stream);
+lsnif_status lsnif_query_host_wire(lsnif_model model, const lsnif_ray* h_rays, int64_t n, int mode,
+                                   lsnif_hit_wire* h_hits, void* stream);
+/* Host-side expansion of wire records into lsnif_hit records, no device needed. */
+lsnif_status lsnif_hits_from_wire(const lsnif_hit_wire* h_wire, int64_t n, lsnif_hit* h_out);
 
 /* Replaces infer_batch (renderer.cpp:183-226): `inputs` is the reference's
  * MatX inputs(input_width, n) column-major fp32 (DEVICE), intervals n

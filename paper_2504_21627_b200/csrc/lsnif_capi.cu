@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -73,12 +74,6 @@ float half_bits_to_float(uint16_t h) {  // IEEE binary16 -> fp32 (exact)
   return f;
 }
 
-uint16_t float_to_half_bits(float v) {  // exact for the powers of two used here
-  const __half h = __float2half_rn(v);
-  uint16_t b;
-  std::memcpy(&b, &h, 2);
-  return b;
-}
 
 // ------------------------------------------------------------- workspace
 struct Workspace {
@@ -89,7 +84,10 @@ struct Workspace {
   uint8_t* counters = nullptr;  // per chunk: u64 batch counter + one i32 row counter per K bin
   unsigned long long* stats = nullptr;
   int64_t last_rays = 0;
-  // profiling: event pairs around each launch (kind 0 trace, 1 mlp)
+  // profiling: event pairs around each launch (kind 0 trace, 1 mlp). The
+  // query thread appends and lsnif_profile_read (any thread) drains them:
+  // both hold prof_mu.
+  std::mutex prof_mu;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
   uint64_t launches[2] = {0, 0};
@@ -213,13 +211,15 @@ struct lsnif_model_s {
   std::mutex mu;
   std::map<cudaStream_t, std::unique_ptr<Workspace>> ws;
   std::unique_ptr<HostStaging> staging;
+  std::unique_ptr<HostStagingT<lsnif_hit_wire>> staging_wire;
   std::mutex staging_mu;
-  bool profiling = false;
+  std::atomic<bool> profiling{false};
 
   ~lsnif_model_s() {
     cudaSetDevice(device);
     ws.clear();
     staging.reset();
+    staging_wire.reset();
     for (void* p : allocations) cudaFree(p);
   }
 
@@ -621,8 +621,10 @@ void create_into(const lsnif_model_desc& d, int device, lsnif_model* out) {
 }
 
 // n is the ray count, or its upper bound when n_dev (device-side count) is set.
-void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, lsnif_hit* d_hits,
-               cudaStream_t st, const int32_t* n_dev = nullptr, const lsnif_interval* d_intervals = nullptr) {
+// wire: d_hits holds lsnif_hit_wire records (16 B) instead of lsnif_hit.
+void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, void* d_hits,
+               cudaStream_t st, const int32_t* n_dev = nullptr, const lsnif_interval* d_intervals = nullptr,
+               bool wire = false) {
   if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
   if (mode != LSNIF_QUERY_CLOSEST && mode != LSNIF_QUERY_ANY) fail(LSNIF_INVALID_ARGUMENT, "bad query mode");
   if (n > 0 && (!d_rays || !d_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
@@ -644,7 +646,9 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     tp.n_dev = n_dev;
     tp.offset = s;
     tp.mode = mode;
-    tp.out = d_hits + s;
+    const size_t rec = wire ? sizeof(lsnif_hit_wire) : sizeof(lsnif_hit);
+    tp.out = static_cast<uint8_t*>(d_hits) + s * rec;
+    tp.wire = wire ? 1 : 0;
     tp.X = w.X;
     tp.meta = w.meta;
     uint8_t* cc = w.counters + kChunkCounterBytes * ci;
@@ -652,41 +656,40 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, l
     tp.row_counter = reinterpret_cast<int32_t*>(cc + 8);
     tp.cap_tiles = static_cast<int64_t>(w.x_tiles);
     tp.stats = w.stats;
+    // one read of the flag per chunk; the event bookkeeping under prof_mu
+    const bool prof = M.profiling.load(std::memory_order_relaxed);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (M.profiling) {
-      e0 = w.take_event();
-      ck(cudaEventRecord(e0, st), "cudaEventRecord");
-    }
+    auto record = [&](cudaEvent_t& e) {
+      std::lock_guard<std::mutex> lk(w.prof_mu);
+      e = w.take_event();
+      ck(cudaEventRecord(e, st), "cudaEventRecord");
+    };
+    auto finish = [&](int kind) {
+      std::lock_guard<std::mutex> lk(w.prof_mu);
+      ++w.launches[kind];
+      if (prof) w.ev_used.push_back({kind, {e0, e1}});
+    };
+    if (prof) record(e0);
     ck(lsnif_dev::launch_trace(tp, false, st), "trace_encode_kernel");
-    ++w.launches[0];
-    if (M.profiling) {
-      e1 = w.take_event();
-      ck(cudaEventRecord(e1, st), "cudaEventRecord");
-      w.ev_used.push_back({0, {e0, e1}});
-    }
+    if (prof) record(e1);
+    finish(0);
     lsnif_dev::MlpParams mp{};
     mp.m = M.dm;
     mp.X = w.X;
     mp.meta = w.meta;
     mp.row_counter = reinterpret_cast<int32_t*>(cc + 8);
     mp.cap_tiles = static_cast<int64_t>(w.x_tiles);
-    mp.out = d_hits + s;
+    mp.out = static_cast<uint8_t*>(d_hits) + s * rec;
+    mp.wire = wire ? 1 : 0;
     mp.mode = mode;
     mp.n_dev = n_dev;
     mp.offset = s;
 
-    if (M.profiling) {
-      e0 = w.take_event();
-      ck(cudaEventRecord(e0, st), "cudaEventRecord");
-    }
+    if (prof) record(e0);
     ck(lsnif_dev::launch_mlp(mp, static_cast<int>((cn + kTileM - 1) / kTileM) + M.dm.n_bins, M.num_sms, st),
        "mlp_tc_kernel");
-    ++w.launches[1];
-    if (M.profiling) {
-      e1 = w.take_event();
-      ck(cudaEventRecord(e1, st), "cudaEventRecord");
-      w.ev_used.push_back({1, {e0, e1}});
-    }
+    if (prof) record(e1);
+    finish(1);
   }
 }
 
@@ -1079,6 +1082,37 @@ lsnif_status lsnif_query_host(lsnif_model model, const lsnif_ray* h_rays, int64_
   });
 }
 
+lsnif_status lsnif_query_wire(lsnif_model model, const lsnif_ray* d_rays, int64_t n, int mode,
+                              lsnif_hit_wire* d_hits, void* stream) {
+  return guarded([&] {
+    check_model(model);
+    run_query(*model, d_rays, n, mode, d_hits, static_cast<cudaStream_t>(stream), nullptr, nullptr, true);
+  });
+}
+
+lsnif_status lsnif_query_host_wire(lsnif_model model, const lsnif_ray* h_rays, int64_t n, int mode,
+                                   lsnif_hit_wire* h_hits, void* stream) {
+  return guarded([&] {
+    check_model(model);
+    if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative ray count");
+    if (n > 0 && (!h_rays || !h_hits)) fail(LSNIF_INVALID_ARGUMENT, "null ray or hit pointer");
+    ck(cudaSetDevice(model->device), "cudaSetDevice");
+    std::lock_guard<std::mutex> lock(model->staging_mu);
+    host_round_trip(model->staging_wire, kHostChunk, h_rays, n, h_hits, static_cast<cudaStream_t>(stream),
+                    [&](const lsnif_ray* r, int64_t cn, lsnif_hit_wire* h, cudaStream_t st) {
+                      run_query(*model, r, cn, mode, h, st, nullptr, nullptr, true);
+                    });
+  });
+}
+
+lsnif_status lsnif_hits_from_wire(const lsnif_hit_wire* h_wire, int64_t n, lsnif_hit* h_out) {
+  return guarded([&] {
+    if (n < 0) fail(LSNIF_INVALID_ARGUMENT, "negative count");
+    if (n > 0 && (!h_wire || !h_out)) fail(LSNIF_INVALID_ARGUMENT, "null pointer");
+    for (int64_t i = 0; i < n; ++i) lsnif_dev::wire_unpack(h_wire[i], h_out[i]);
+  });
+}
+
 lsnif_status lsnif_infer_batch(lsnif_model model, const float* d_inputs, int64_t rows, int64_t n,
                                const lsnif_interval* d_intervals, int64_t n_intervals,
                                lsnif_hit* d_hits, void* stream) {
@@ -1135,7 +1169,7 @@ lsnif_status lsnif_debug_traverse(lsnif_model model, const lsnif_ray* d_rays, in
 lsnif_status lsnif_profile_enable(lsnif_model model, int enable) {
   return guarded([&] {
     check_model(model);
-    model->profiling = enable != 0;
+    model->profiling.store(enable != 0);
   });
 }
 
@@ -1150,6 +1184,7 @@ lsnif_status lsnif_profile_read(lsnif_model model, void* stream, int reset, lsni
       if (stream && kv.first != static_cast<cudaStream_t>(stream)) continue;
       Workspace& w = *kv.second;
       ck(cudaStreamSynchronize(kv.first), "cudaStreamSynchronize");
+      std::lock_guard<std::mutex> plk(w.prof_mu);
       out->trace_launches += w.launches[0];
       out->mlp_launches += w.launches[1];
       for (auto& u : w.ev_used) {

@@ -560,6 +560,83 @@ __device__ __forceinline__ void store_hit(lsnif_hit* dst, const lsnif_hit& h) {
   d4[1] = make_float4(h.normal[2], h.albedo[0], h.albedo[1], h.albedo[2]);
 }
 
+// ------------------------------------------------------------ wire form
+
+// Packed 16 B result (lsnif_hit_wire, include/lsnif_gpu.h). The normal is
+// the octahedral map of the unit vector (|x| + |y| + |z| = 1 projection,
+// lower hemisphere folded) quantised to 2 x snorm16; the albedo 3 x unorm10.
+// Host and device share the code (the host decode expands query results).
+__host__ __device__ __forceinline__ float wire_sign(float v) { return v >= 0.0f ? 1.0f : -1.0f; }
+
+__host__ __device__ __forceinline__ uint32_t wire_snorm16(float v) {
+  v = v < -1.0f ? -1.0f : (v > 1.0f ? 1.0f : v);
+  const int q = static_cast<int>(rintf(v * 32767.0f));
+  return static_cast<uint32_t>(q) & 0xffffu;
+}
+
+__host__ __device__ __forceinline__ uint32_t wire_unorm10(float v) {
+  v = v < 0.0f ? 0.0f : (v > 1.0f ? 1.0f : v);
+  return static_cast<uint32_t>(rintf(v * 1023.0f));
+}
+
+__host__ __device__ __forceinline__ void wire_pack_normal_albedo(const float n[3], const float a[3],
+                                                                 uint32_t& normal_oct, uint32_t& albedo) {
+  const float l1 = fabsf(n[0]) + fabsf(n[1]) + fabsf(n[2]);
+  uint32_t zero = 0u;
+  float u = 0.0f, v = 0.0f;
+  if (l1 > 0.0f) {
+    u = n[0] / l1;
+    v = n[1] / l1;
+    if (n[2] < 0.0f) {
+      const float uu = (1.0f - fabsf(v)) * wire_sign(u);
+      const float vv = (1.0f - fabsf(u)) * wire_sign(v);
+      u = uu;
+      v = vv;
+    }
+  } else {
+    zero = LSNIF_WIRE_ZERO_NORMAL;
+  }
+  normal_oct = wire_snorm16(u) | (wire_snorm16(v) << 16);
+  albedo = wire_unorm10(a[0]) | (wire_unorm10(a[1]) << 10) | (wire_unorm10(a[2]) << 20) | zero;
+}
+
+__host__ __device__ __forceinline__ void wire_unpack(const lsnif_hit_wire& w, lsnif_hit& h) {
+  h.flags_material = w.flags_material;
+  h.t_world = w.t_world;
+  const float u = fmaxf(static_cast<float>(static_cast<int16_t>(w.normal_oct & 0xffffu)) / 32767.0f, -1.0f);
+  const float v = fmaxf(static_cast<float>(static_cast<int16_t>(w.normal_oct >> 16)) / 32767.0f, -1.0f);
+  if (w.albedo_unorm & LSNIF_WIRE_ZERO_NORMAL) {
+    h.normal[0] = h.normal[1] = h.normal[2] = 0.0f;
+  } else {
+    float x = u, y = v;
+    const float z = 1.0f - fabsf(u) - fabsf(v);
+    if (z < 0.0f) {
+      x = (1.0f - fabsf(v)) * wire_sign(u);
+      y = (1.0f - fabsf(u)) * wire_sign(v);
+    }
+    const float len = sqrtf(x * x + y * y + z * z);
+    h.normal[0] = x / len;
+    h.normal[1] = y / len;
+    h.normal[2] = z / len;
+  }
+  for (int c = 0; c < 3; ++c) h.albedo[c] = static_cast<float>((w.albedo_unorm >> (10 * c)) & 1023u) / 1023.0f;
+}
+
+__device__ __forceinline__ void store_hit_wire(lsnif_hit_wire* dst, const lsnif_hit& h) {
+  uint32_t no, al;
+  wire_pack_normal_albedo(h.normal, h.albedo, no, al);
+  *reinterpret_cast<uint4*>(dst) = make_uint4(h.flags_material, __float_as_uint(h.t_world), no, al);
+}
+
+// One result into the caller's array: the 32 B parity record or the 16 B
+// wire record.
+__device__ __forceinline__ void store_result(void* out, int64_t i, bool wire, const lsnif_hit& h) {
+  if (wire)
+    store_hit_wire(static_cast<lsnif_hit_wire*>(out) + i, h);
+  else
+    store_hit(static_cast<lsnif_hit*>(out) + i, h);
+}
+
 // Byte offset of element (row, col) of an fp16 operand tile in the UMMA
 // K-major no-swizzle canonical layout: 8x8 core matrices (128 B), rows
 // grouped by 8 at stride 128 B (SBO), K chunks of 8 at stride rows*16 B (LBO).

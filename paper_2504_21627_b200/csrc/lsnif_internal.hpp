@@ -34,7 +34,8 @@ struct TraceParams {
   const int32_t* n_dev;       // optional device-side ray count of the whole query
   int64_t offset;             // first ray of this launch within the query
   int mode;
-  lsnif_hit* out;
+  void* out;                  // lsnif_hit[] or (wire) lsnif_hit_wire[]
+  int wire;
   uint8_t* X;                 // compacted MLP operand tiles, per K bin (bin_x_offset)
   RowMeta* meta;              // bin b's rows at meta + b * cap_tiles * 128
   int32_t* row_counter;       // one per K bin
@@ -57,7 +58,8 @@ struct MlpParams {
   const RowMeta* meta;
   const int32_t* row_counter;  // one per K bin
   int64_t cap_tiles;
-  lsnif_hit* out;
+  void* out;             // lsnif_hit[] or (wire) lsnif_hit_wire[]
+  int wire;
   int mode;
   const int32_t* n_dev;  // optional device-side ray count of the query (as TraceParams)
   int64_t offset;        // first ray of this chunk within the query

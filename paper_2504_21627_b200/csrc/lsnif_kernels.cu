@@ -73,7 +73,6 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
   };
   auto pool_get = [&](int i) -> uint2 { return make_uint2(__float_as_uint(pool_t[i]), pool_c[i]); };
   const float scale = m.act_scale;
-  const int64_t nbatch = (P.n + 127) / 128;
   uint32_t st_pair = 0, st_rows = 0, st_pts = 0, st_vol = 0;  // query statistics
   const int64_t n_rays = P.n_dev ? max(static_cast<int64_t>(0), min(P.n, static_cast<int64_t>(*P.n_dev) - P.offset))
                                  : P.n;
@@ -198,11 +197,11 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
     if (!DEBUG) {
       if (live && !pair) {
         lsnif_hit h{};
-        store_hit(P.out + ray_idx, h);
+        store_result(P.out, ray_idx, P.wire, h);
       } else if (pair && count == 0) {
         lsnif_hit h;
         decode_zero(m, enter, exit, t_min, t_max, P.mode, h);
-        store_hit(P.out + ray_idx, h);
+        store_result(P.out, ray_idx, P.wire, h);
       }
     } else if (live) {
       P.info[ray_idx] = pair ? (count | (fio ? 1 << 8 : 0) | (1 << 9)) : 0;
@@ -710,11 +709,12 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
     // warps of a row split the work: lower half z0, z1, z8.. (visibility,
     // t_world, material, accept), upper half z2..z7 (normal, albedo).
     float* zs = zslots + (warp - 2) * kZSlots * 32 + lane;
-    float4 pa, pb;  // pending tile's metadata
+    float4 pa = make_float4(0.f, 0.f, 0.f, 0.f), pb = pa;  // pending tile's metadata
     bool plive = false;
     auto decode_pending = [&]() {
       if (!plive) return;
-      float* dst = reinterpret_cast<float*>(P.out + __float_as_int(pa.x));
+      const int64_t ray = __float_as_int(pa.x);
+      float* dst = reinterpret_cast<float*>(static_cast<uint8_t*>(P.out) + ray * (P.wire ? 16 : 32));
       if (half == 0) {
         float zm[8];
 #pragma unroll
@@ -727,8 +727,14 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
         float nrm[3], alb[3];
         decode_normal(zs[0], zs[32], zs[64], nrm);
         decode_albedo(zs[96], zs[128], zs[160], alb);
-        *reinterpret_cast<float2*>(dst + 2) = make_float2(nrm[0], nrm[1]);
-        *reinterpret_cast<float4*>(dst + 4) = make_float4(nrm[2], alb[0], alb[1], alb[2]);
+        if (P.wire) {
+          uint32_t no, al;
+          wire_pack_normal_albedo(nrm, alb, no, al);
+          *reinterpret_cast<uint2*>(dst + 2) = make_uint2(no, al);
+        } else {
+          *reinterpret_cast<float2*>(dst + 2) = make_float2(nrm[0], nrm[1]);
+          *reinterpret_cast<float4*>(dst + 4) = make_float4(nrm[2], alb[0], alb[1], alb[2]);
+        }
       }
       plive = false;
     };
@@ -1260,16 +1266,19 @@ static cudaError_t launch_trace_t(const TraceParams& p, cudaStream_t st) {
   const size_t smem = trace_smem_bytes(p.m, TW);
   thread_local LaunchCfg cfg;
   int dev = 0;
-  cudaGetDevice(&dev);
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
   if (cfg.dev != dev || cfg.smem != smem) {
-    cudaError_t e = ensure_smem(kern, smem);
+    e = ensure_smem(kern, smem);
     if (e != cudaSuccess) return e;
     if (const char* c = std::getenv("LSNIF_TRACE_CARVEOUT")) {  // A/B probe: shared-memory share (%)
       e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(c));
       if (e != cudaSuccess) return e;
     }
-    cudaDeviceGetAttribute(&cfg.sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.per_sm, kern, 32 * TW, smem);
+    e = cudaDeviceGetAttribute(&cfg.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cfg.per_sm, kern, 32 * TW, smem);
+    if (e != cudaSuccess) return e;
     if (const char* c = std::getenv("LSNIF_TRACE_BLOCKS")) cfg.per_sm = std::min(cfg.per_sm, std::atoi(c));
     cfg.dev = dev;
     cfg.smem = smem;
@@ -1302,7 +1311,8 @@ static cudaError_t launch_mlp_t(const MlpParams& p, int max_tiles, int num_sms, 
   const unsigned grid = static_cast<unsigned>(std::min(max_tiles, num_sms));
   thread_local LaunchCfg c;
   int dev = 0;
-  cudaGetDevice(&dev);
+  cudaError_t de = cudaGetDevice(&dev);
+  if (de != cudaSuccess) return de;
   if (c.dev != dev || c.smem != smem) {
     cudaError_t e = ensure_smem(mlp_tc_kernel<HID, NS>, smem);
     if (e != cudaSuccess) return e;

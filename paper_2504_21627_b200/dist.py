@@ -31,7 +31,10 @@ def gather_to_rank0(local, group=None, out=None, sizes=None):
     `sizes` (per-rank row counts, e.g. from row_band) skips the size
     exchange; `out` (rank 0, shape (sum(sizes),) + local.shape[1:]) is
     filled in place, so a caller that preallocates it keeps allocations out
-    of its timed loop."""
+    of its timed loop. Ranks with zero rows post no operation (every rank
+    with rows joins the same single batch_isend_irecv; a communicator's
+    first P2P call should therefore come from a batch in which all ranks
+    take part — callers with empty bands warm up with a full batch first)."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -41,12 +44,16 @@ def gather_to_rank0(local, group=None, out=None, sizes=None):
         gathered = [torch.zeros_like(n) for _ in range(world)]
         dist.all_gather(gathered, n, group=group)
         sizes = [int(x.item()) for x in gathered]
+    if len(sizes) != world or local.shape[0] != sizes[rank]:
+        raise ValueError(f"rank {rank}: {local.shape[0]} local rows but sizes = {sizes}")
     if rank != 0:
         if sizes[rank]:
             dist.batch_isend_irecv([dist.P2POp(dist.isend, local.contiguous(), 0, group)])[0].wait()
         return None
     if out is None:
         out = torch.empty((sum(sizes),) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    elif out.shape != (sum(sizes),) + tuple(local.shape[1:]) or out.dtype != local.dtype:
+        raise ValueError("out must hold sum(sizes) rows of local's dtype and row shape")
     offs = [0]
     for x in sizes:
         offs.append(offs[-1] + x)
@@ -55,3 +62,42 @@ def gather_to_rank0(local, group=None, out=None, sizes=None):
     for req in (dist.batch_isend_irecv(ops) if ops else []):
         req.wait()
     return out
+
+
+def piece_range(band: int, pieces: int, k: int) -> tuple[int, int]:
+    """Rows [s, e) of piece k when a band of `band` rows is computed in
+    `pieces` consecutive pieces (the unit of compute / gather overlap)."""
+    return row_band(band, pieces, k)
+
+
+def gather_piece_to_rank0(local_piece, k: int, pieces: int, sizes, out=None, group=None):
+    """Piece k of every rank's band into rank 0's full-frame `out` (rows in
+    rank order; rank r's band starts at sum(sizes[:r])). Rank 0 computes its
+    own band in place inside `out`, so only ranks 1.. transfer: each sends its
+    piece k point-to-point into its slice of rank 0's output (one batched
+    isend / irecv set per piece). Called by every rank for k = 0 .. pieces-1
+    in order, typically on a communication stream right after piece k's
+    compute, so the transfer of piece k overlaps the compute of piece k + 1
+    (SURVEY.md §8(e)). Returns the async work handles (empty when this rank
+    has nothing to move)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if len(sizes) != world:
+        raise ValueError(f"sizes has {len(sizes)} entries for world size {world}")
+    if rank != 0:
+        s, e = piece_range(sizes[rank], pieces, k)
+        if local_piece.shape[0] != e - s:
+            raise ValueError(f"rank {rank} piece {k}: {local_piece.shape[0]} rows, expected {e - s}")
+        if e == s:
+            return []
+        return dist.batch_isend_irecv([dist.P2POp(dist.isend, local_piece, 0, group)])
+    if out is None or out.shape[0] != sum(sizes):
+        raise ValueError("rank 0 needs the full-frame output (sum(sizes) rows)")
+    off, ops = sizes[0], []
+    for r in range(1, world):
+        s, e = piece_range(sizes[r], pieces, k)
+        if e > s:
+            ops.append(dist.P2POp(dist.irecv, out[off + s:off + e], r, group))
+        off += sizes[r]
+    return dist.batch_isend_irecv(ops) if ops else []

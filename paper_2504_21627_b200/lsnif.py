@@ -26,6 +26,10 @@ LIB_PATH = os.environ.get("LSNIF_LIB") or os.path.join(HERE, "liblsnif_gpu.so") 
 RAY_DTYPE = np.dtype([("o", "<f4", 3), ("d", "<f4", 3), ("t_min", "<f4"), ("t_max", "<f4")])
 HIT_DTYPE = np.dtype([("flags_material", "<u4"), ("t_world", "<f4"), ("normal", "<f4", 3),
                       ("albedo", "<f4", 3)])
+# lsnif_hit_wire: packed 16 B result (octahedral snorm16 normal, unorm10 albedo)
+WIRE_DTYPE = np.dtype([("flags_material", "<u4"), ("t_world", "<f4"), ("normal_oct", "<u4"),
+                       ("albedo_unorm", "<u4")])
+WIRE_ZERO_NORMAL = 0x40000000
 SCENE_HIT_DTYPE = np.dtype([("t", "<f4"), ("position", "<f4", 3), ("normal", "<f4", 3),
                             ("albedo", "<f4", 3), ("kind", "<u4"), ("roughness", "<f4"),
                             ("object_index", "<i4"), ("flags", "<u4"), ("pad", "<u4", 2)])
@@ -77,6 +81,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.lsnif_model_get_info.argtypes = [P, C.POINTER(ModelInfo)]
     lib.lsnif_query.argtypes = [P, P, C.c_int64, C.c_int, P, P]
     lib.lsnif_query_host.argtypes = [P, P, C.c_int64, C.c_int, P, P]
+    lib.lsnif_query_wire.argtypes = [P, P, C.c_int64, C.c_int, P, P]
+    lib.lsnif_query_host_wire.argtypes = [P, P, C.c_int64, C.c_int, P, P]
+    lib.lsnif_hits_from_wire.argtypes = [P, C.c_int64, P]
     lib.lsnif_query_pairs.argtypes = [P, P, P, C.c_int64, C.c_int, P, P]
     lib.lsnif_query_closest.argtypes = [P, P, P, C.c_int64, P, P]
     lib.lsnif_query_any.argtypes = [P, P, P, C.c_int64, P, P]
@@ -98,7 +105,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.lsnif_trainer_batch_grad.argtypes = [P, P, P, C.c_int64, P, P, P, P]
     lib.lsnif_trainer_sample.argtypes = [P, C.c_int64, C.c_int64, P, P, P]
     for name in ("lsnif_model_load", "lsnif_model_destroy", "lsnif_model_get_info", "lsnif_query",
-                 "lsnif_query_host", "lsnif_query_pairs", "lsnif_query_closest", "lsnif_query_any",
+                 "lsnif_query_host", "lsnif_query_wire", "lsnif_query_host_wire",
+                 "lsnif_hits_from_wire", "lsnif_query_pairs", "lsnif_query_closest", "lsnif_query_any",
                  "lsnif_infer_batch", "lsnif_debug_traverse",
                  "lsnif_last_query_stats", "lsnif_profile_enable", "lsnif_profile_read",
                  "lsnif_scene_create", "lsnif_scene_destroy", "lsnif_scene_query",
@@ -123,6 +131,30 @@ def _check(st: int) -> None:
 def _torch():
     import torch
     return torch
+
+
+def _check_rays(rays):
+    """Query input: a contiguous (n, 8) float32 CUDA tensor (lsnif_ray records).
+    No implicit copy: a temporary could be freed before an asynchronous
+    launch on another stream reads it."""
+    torch = _torch()
+    if not (rays.is_cuda and rays.dtype == torch.float32 and rays.dim() == 2 and rays.shape[1] == 8):
+        raise ValueError("rays must be an (n, 8) float32 CUDA tensor")
+    if not rays.is_contiguous():
+        raise ValueError("rays must be contiguous")
+    return rays
+
+
+def _check_out(out, shape, device):
+    """Query output: allocated when None, else an int32 contiguous tensor of
+    `shape` on `device` (an undersized buffer would be written out of bounds)."""
+    torch = _torch()
+    if out is None:
+        return torch.empty(shape, dtype=torch.int32, device=device)
+    if out.dtype != torch.int32 or tuple(out.shape) != tuple(shape) or out.device != device \
+            or not out.is_contiguous():
+        raise ValueError(f"out must be a contiguous int32 tensor of shape {tuple(shape)} on {device}")
+    return out
 
 
 def _stream_ptr(stream) -> int:
@@ -163,14 +195,22 @@ class GpuModel:
     def query(self, rays, mode: int = CLOSEST, out=None, stream=None):
         """rays: CUDA tensor (n, 8) float32 (lsnif_ray records). Returns (n, 8)
         int32 tensor of lsnif_hit records (view with hits_to_numpy)."""
-        torch = _torch()
-        assert rays.is_cuda and rays.dtype == torch.float32 and rays.shape[-1] == 8
-        rays = rays.contiguous()
+        rays = _check_rays(rays)
         n = rays.shape[0]
-        if out is None:
-            out = torch.empty((n, 8), dtype=torch.int32, device=rays.device)
+        out = _check_out(out, (n, 8), rays.device)
         _check(load_library().lsnif_query(self.h, rays.data_ptr(), n, mode, out.data_ptr(),
                                           _stream_ptr(stream)))
+        return out
+
+    def query_wire(self, rays, mode: int = CLOSEST, out=None, stream=None):
+        """lsnif_query_wire: (n, 4) int32 tensor of packed 16 B lsnif_hit_wire
+        records (wire_to_hits expands them)."""
+        torch = _torch()
+        rays = _check_rays(rays)
+        n = rays.shape[0]
+        out = _check_out(out, (n, 4), rays.device)
+        _check(load_library().lsnif_query_wire(self.h, rays.data_ptr(), n, mode, out.data_ptr(),
+                                               _stream_ptr(stream)))
         return out
 
     def query_pairs(self, rays, intervals, mode: int = CLOSEST, out=None, stream=None):
@@ -178,12 +218,12 @@ class GpuModel:
         given [t_enter, t_exit] (CUDA tensor (n, 2) float32) instead of the
         in-kernel frame clip. Returns (n, 8) int32 lsnif_hit records."""
         torch = _torch()
-        assert rays.is_cuda and rays.dtype == torch.float32 and rays.shape[-1] == 8
-        assert intervals.is_cuda and intervals.dtype == torch.float32 and tuple(intervals.shape) == (rays.shape[0], 2)
-        rays, intervals = rays.contiguous(), intervals.contiguous()
+        rays = _check_rays(rays)
+        if not (intervals.is_cuda and intervals.dtype == torch.float32 and intervals.is_contiguous()
+                and tuple(intervals.shape) == (rays.shape[0], 2) and intervals.device == rays.device):
+            raise ValueError("intervals must be a contiguous (n, 2) float32 tensor on the rays' device")
         n = rays.shape[0]
-        if out is None:
-            out = torch.empty((n, 8), dtype=torch.int32, device=rays.device)
+        out = _check_out(out, (n, 8), rays.device)
         _check(load_library().lsnif_query_pairs(self.h, rays.data_ptr(), intervals.data_ptr(), n, mode,
                                                 out.data_ptr(), _stream_ptr(stream)))
         return out
@@ -246,6 +286,23 @@ class GpuModel:
             out = np.empty(n, HIT_DTYPE)
         _check(load_library().lsnif_query_host(self.h, rays.ctypes.data, n, mode, out.ctypes.data,
                                                None))
+        return out
+
+    def query_host_wire(self, rays, mode: int = CLOSEST, out=None):
+        """lsnif_query_host_wire: host rays (RAY_DTYPE / (n, 8) float32 array or
+        pinned CPU tensor) -> WIRE_DTYPE records (or the given (n, 4) int32
+        CPU tensor / WIRE_DTYPE array)."""
+        if hasattr(rays, "data_ptr"):
+            n, src = rays.shape[0], rays.data_ptr()
+        else:
+            rays = np.ascontiguousarray(rays)
+            if rays.dtype != RAY_DTYPE:
+                rays = rays.astype(np.float32, copy=False).reshape(-1, 8)
+            n, src = len(rays), rays.ctypes.data
+        if out is None:
+            out = np.empty(n, WIRE_DTYPE)
+        dst = out.data_ptr() if hasattr(out, "data_ptr") else out.ctypes.data
+        _check(load_library().lsnif_query_host_wire(self.h, src, n, mode, dst, None))
         return out
 
     def intersect(self, rays: np.ndarray) -> np.ndarray:
@@ -327,11 +384,9 @@ class GpuScene:
     def query(self, rays, mode: int = CLOSEST, out=None, stream=None):
         """World-space CUDA rays (n, 8) -> (n, 16) int32 tensor of
         lsnif_scene_hit records (view with scene_hits_to_numpy)."""
-        torch = _torch()
-        rays = rays.contiguous()
+        rays = _check_rays(rays)
         n = rays.shape[0]
-        if out is None:
-            out = torch.empty((n, 16), dtype=torch.int32, device=rays.device)
+        out = _check_out(out, (n, 16), rays.device)
         _check(load_library().lsnif_scene_query(self.h, rays.data_ptr(), n, mode, out.data_ptr(),
                                                 _stream_ptr(stream)))
         return out
@@ -407,6 +462,16 @@ def hits_to_numpy(hits) -> np.ndarray:
     """(n, 8) int32 CUDA/CPU tensor of lsnif_hit -> numpy HIT_DTYPE records."""
     a = hits.detach().cpu().numpy() if hasattr(hits, "detach") else np.asarray(hits)
     return np.ascontiguousarray(a).view(HIT_DTYPE).reshape(-1)
+
+
+def wire_to_hits(wire) -> np.ndarray:
+    """Packed wire records ((n, 4) int32 tensor / WIRE_DTYPE array) -> HIT_DTYPE
+    records, expanded by the library's host decode (lsnif_hits_from_wire)."""
+    a = wire.detach().cpu().numpy() if hasattr(wire, "detach") else np.asarray(wire)
+    a = np.ascontiguousarray(a).view(WIRE_DTYPE).reshape(-1)
+    out = np.empty(len(a), HIT_DTYPE)
+    _check(load_library().lsnif_hits_from_wire(a.ctypes.data, len(a), out.ctypes.data))
+    return out
 
 
 def rays_to_tensor(rays: np.ndarray, device="cuda"):

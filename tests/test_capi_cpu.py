@@ -106,3 +106,44 @@ def test_render_and_trainer_fail_loudly_without_gpu_work(tmp_path):
                                             ctypes.byref(tc), 0, ctypes.byref(h))
     assert st == lsnif.RUNTIME_ERROR and b"cannot open model file" in lib.lsnif_last_error()
     assert lib.lsnif_trainer_step(None, 1, None, None) == lsnif.INVALID_ARGUMENT
+
+
+def _oct_pack(n: np.ndarray) -> np.ndarray:
+    """Independent numpy statement of the octahedral snorm16 normal map."""
+    n = n.astype(np.float64)
+    l1 = np.abs(n).sum(axis=1, keepdims=True)
+    p = n[:, :2] / l1
+    neg = n[:, 2] < 0
+    sgn = np.where(p >= 0, 1.0, -1.0)
+    p[neg] = ((1 - np.abs(p[neg][:, ::-1])) * sgn[neg])
+    q = np.rint(np.clip(p, -1, 1) * 32767).astype(np.int64) & 0xFFFF
+    return (q[:, 0] | (q[:, 1] << 16)).astype(np.uint32)
+
+
+def test_wire_records_decode_within_tolerance():
+    """lsnif_hits_from_wire (host decode of the packed 16 B result): flags and
+    t bit-identical, normals within 0.01 degree, albedo within half a unorm10 step, the
+    zero-normal marker honoured (SURVEY App. B tolerances: 1 degree, 2e-3)."""
+    assert lsnif.WIRE_DTYPE.itemsize == 16
+    rng = np.random.default_rng(7)
+    n = 20000
+    nrm = rng.normal(size=(n, 3))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    nrm[:6] = [[0, 0, 1], [0, 0, -1], [1, 0, 0], [0, -1, 0], [-1, 0, 0], [0.6, -0.8, 0]]
+    alb = rng.uniform(size=(n, 3)).astype(np.float32)
+    w = np.zeros(n, lsnif.WIRE_DTYPE)
+    w["flags_material"] = rng.integers(0, 8, n) | (rng.integers(0, 8, n) << 8)
+    w["t_world"] = rng.uniform(0, 5, n).astype(np.float32)
+    w["normal_oct"] = _oct_pack(nrm)
+    q = np.rint(alb.astype(np.float64) * 1023).astype(np.uint32)
+    w["albedo_unorm"] = q[:, 0] | (q[:, 1] << 10) | (q[:, 2] << 20)
+    w["albedo_unorm"][-1] |= lsnif.WIRE_ZERO_NORMAL
+    h = lsnif.wire_to_hits(w)
+    assert np.array_equal(h["flags_material"], w["flags_material"])
+    assert np.array_equal(h["t_world"].view(np.uint32), w["t_world"].view(np.uint32))
+    got = h["normal"][:-1].astype(np.float64)
+    assert np.allclose(np.linalg.norm(got, axis=1), 1.0, atol=1e-6)
+    ang = np.degrees(np.arctan2(np.linalg.norm(np.cross(got, nrm[:-1]), axis=1), np.sum(got * nrm[:-1], axis=1)))
+    assert ang.max() < 0.01, ang.max()
+    assert np.abs(h["albedo"] - alb).max() <= 0.5 / 1023 + 1e-7
+    assert np.all(h["normal"][-1] == 0)

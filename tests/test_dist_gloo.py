@@ -50,6 +50,47 @@ def _worker(rank, world, port, out_path):
     dist.destroy_process_group()
 
 
+def _piece_worker(rank, world, port, out_path, total, pieces):
+    """The bench's C5 form: each rank's band in `pieces` pieces, piece k of
+    every rank gathered into rank 0's full frame right after it is computed
+    (rank 0's own band written in place)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2504_21627_b200 import dist as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bands = [D.ray_range(total, world, r) for r in range(world)]
+    sizes = [e - s for s, e in bands]
+    s0, band = bands[rank][0], sizes[rank]
+    frame = torch.full((total, 4), -1, dtype=torch.int32) if rank == 0 else None
+    local = frame[:band] if rank == 0 else torch.empty((band, 4), dtype=torch.int32)
+    for k in range(pieces):
+        ps, pe = D.piece_range(band, pieces, k)
+        # "compute": a record that names its global ray index
+        local[ps:pe] = torch.arange(s0 + ps, s0 + pe, dtype=torch.int32).reshape(-1, 1) * 4 + \
+            torch.arange(4, dtype=torch.int32)
+        for w in D.gather_piece_to_rank0(local[ps:pe], k, pieces, sizes, out=frame):
+            w.wait()
+    if rank == 0:
+        np.save(out_path, frame.numpy())
+    else:
+        import pytest
+        with pytest.raises(ValueError):  # a piece of the wrong length is refused, not sent
+            D.gather_piece_to_rank0(local[:1], 0, pieces, sizes) if band > 1 else (_ for _ in ()).throw(ValueError())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_piecewise_band_gather(tmp_path):
+    for world, total, pieces in ((2, 1001, 3), (3, 257, 8)):
+        out = str(tmp_path / f"frame_{world}.npy")
+        mp.spawn(_piece_worker, args=(world, _free_port(), out, total, pieces), nprocs=world, join=True)
+        got = np.load(out)
+        ref = np.arange(total * 4, dtype=np.int32).reshape(total, 4)
+        assert np.array_equal(got, ref)
+
+
 def test_row_band_sharding_and_gather(tmp_path):
     out = str(tmp_path / "gathered.npy")
     mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)

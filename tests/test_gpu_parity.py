@@ -368,3 +368,42 @@ def test_cpp_adapter_example_runs():
     assert out.returncode == 0, out.stderr
     assert "rays accepted a neural hit" in out.stdout
     assert "infer_pairs:" in out.stdout and "render 64x36x2" in out.stdout
+
+
+def test_wire_query_matches_parity_layout(gmodel, oracle_teapot):
+    """lsnif_query_wire / lsnif_query_host_wire: flags, material and t_world
+    bit-identical to the 32 B parity records; normal / albedo within the wire
+    encoding's error (< 0.01 degree, <= 0.5/1023) and hence within the App. B
+    gates against the oracle."""
+    rays = W.incoherent_rays(300_000, gmodel.aabb, seed=21)
+    d = lsnif.rays_to_tensor(rays)
+    full = lsnif.hits_to_numpy(gmodel.query(d))
+    wire = gmodel.query_wire(d)
+    assert tuple(wire.shape) == (len(rays), 4)
+    dec = lsnif.wire_to_hits(wire)
+    assert np.array_equal(dec["flags_material"], full["flags_material"])
+    assert np.array_equal(dec["t_world"].view(np.uint32), full["t_world"].view(np.uint32))
+    pair = (full["flags_material"] & 1) == 1
+    nz = pair & (np.sum(full["normal"] ** 2, axis=1) > 0)
+    a, b = dec["normal"][nz].astype(np.float64), full["normal"][nz].astype(np.float64)
+    ang = np.degrees(np.arctan2(np.linalg.norm(np.cross(a, b), axis=1), np.sum(a * b, axis=1)))
+    assert ang.max() < 0.01
+    assert np.all(dec["normal"][pair & ~nz] == 0)
+    assert np.abs(dec["albedo"][pair] - full["albedo"][pair]).max() <= 0.5 / 1023 + 1e-7
+    # host entry point: the same records
+    host = gmodel.query_host_wire(rays)
+    assert host.tobytes() == wire.cpu().numpy().tobytes()
+    # against the oracle through the wire form (App. B gates)
+    ref = oracle_teapot.narrow_phase(rays[:65536], 0, 0)
+    vis, mat, both, dt = compare_query(dec[:65536], ref, "wire")
+    assert vis >= 0.999 and mat >= 0.999
+
+
+def test_query_rejects_bad_output_buffers(gmodel):
+    d = lsnif.rays_to_tensor(W.camera_rays(16, 16))
+    with pytest.raises(ValueError):
+        gmodel.query(d, out=torch.empty((10, 8), dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError):
+        gmodel.query_wire(d, out=torch.empty((256, 8), dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError):
+        gmodel.query(d[:, :6])
