@@ -118,12 +118,11 @@ def build_rays(workload: str, rank: int, box: np.ndarray, world: int = 1):
 
 def c2_shadow_set(primary: np.ndarray, box):
     """The C2 shadow rays, derived ONCE from the CPU reference's own primary
-    hits (oracle narrow phase on the whole frame): every arm answers exactly
-    the same rays (the GPU's fp16 MLP may accept a few different primaries)."""
+    hits (the IEEE build of the reference's narrow phase on the whole frame):
+    every arm answers exactly the same rays (the GPU's fp16 MLP may accept a
+    few different primaries)."""
     from paper_2504_21627_b200 import workloads as W
-    O = cpu_oracle(True)
-    om = O.OracleModel.load(MODEL_PATH, fast=True)
-    hits = om.narrow_phase(primary, 0, 0)
+    hits = parity_model().narrow_phase(primary, 0, 0)
     return W.shadow_rays(primary, hits, box)[0]
 
 
@@ -292,20 +291,73 @@ def cpu_oracle(fast: bool = True):
     return O
 
 
-def time_cpu_sets(model, sets, target_s: float):
-    """Times the CPU reference narrow phase (all host threads) over the ray
-    sets [(rays, mode), ...] answered back to back: one untimed pass, then
-    repeated passes (best of) spanning ~target_s of CPU work. Returns
-    (rays/s, info)."""
+class CpuArm:
+    """The CPU path both CPU legs time (cpu_baseline and --impl reference):
+    the REFERENCE ITSELF when oracle/_ref is built (its own
+    PreparedScene::intersect_scene / occluded_batch, renderer.cpp:269-323,
+    compiled from /root/reference/proj/src against the Eigen-subset shim with
+    the reference's Release flags, called from all host threads on 65,536-ray
+    blocks as render() does: kind "reference"), else the oracle's
+    restatement of the same narrow phase (kind "port")."""
+
+    def __init__(self, path: str = MODEL_PATH):
+        self.kind, self.err = "port", ""
+        try:
+            from oracle import ref as R
+            if not R.available(True):
+                raise RuntimeError("oracle/_ref not built")
+            self.m = R.RefModel(path, fast=True)
+            self.cores = R.hardware_concurrency()
+            self.kind = "reference"
+            self.what = ("the reference's own PreparedScene::intersect_scene / occluded_batch "
+                         "(renderer.cpp:269-323; collect_pairs + run_narrow_phase + infer_batch) compiled "
+                         "from /root/reference/proj/src against the Eigen-subset shim (oracle/_ref), "
+                         "-O3 -march=native, parallel_slices over 65,536-ray blocks on all host threads")
+        except Exception as e:  # the oracle restatement, said so in the line
+            self.err = str(e)[:200]
+            O = cpu_oracle(True)
+            self.m = O.OracleModel.load(path, fast=True)
+            self.cores = int(O.lib(True).oracle_hardware_concurrency())
+            self.what = ("the oracle's C++ restatement of run_narrow_phase + infer_batch (-O3 -march=native, "
+                         "all host threads); oracle/_ref unavailable: " + self.err)
+
+    def run(self, rays, mode: int):
+        if self.kind == "reference":
+            return self.m.scene_query(rays, mode, 0)
+        return self.m.narrow_phase(rays, mode, 0)
+
+    def best_time(self, rays, mode: int, reps: int) -> float:
+        if self.kind == "reference":
+            return self.m.time_scene_query(rays, mode, 0, reps)
+        return self.m.time_narrow_phase(rays, mode, 0, reps)
+
+
+def time_cpu_sets(arm: "CpuArm", sets, target_s: float):
+    """Times the CPU path (all host threads) over the ray sets [(rays, mode),
+    ...] answered back to back: one untimed pass, then repeated passes (best
+    of) spanning ~target_s of CPU work. Returns (rays/s, info)."""
     n = sum(len(r) for r, _ in sets)
     t0 = time.perf_counter()
     for r, mode in sets:
         if len(r):
-            model.narrow_phase(r, mode, 0)
+            arm.run(r, mode)
     one = max(time.perf_counter() - t0, 1e-6)
     reps = max(1, min(200, int(round(target_s / one))))
-    total = sum(model.time_narrow_phase(r, mode, 0, reps) for r, mode in sets if len(r))
+    total = sum(arm.best_time(r, mode, reps) for r, mode in sets if len(r))
     return n / total, {"rays": n, "seconds": reps * total, "reps": reps}
+
+
+def parity_model(path: str = MODEL_PATH):
+    """The IEEE (parity) build of the CPU path for spot checks: the reference
+    itself (oracle/_ref) when built, else the oracle restatement."""
+    try:
+        from oracle import ref as R
+        if R.available(False):
+            return R.RefModel(path)
+    except Exception:
+        pass
+    from oracle import oracle as O
+    return O.OracleModel.load(path)
 
 
 def pairs_fraction(model, rays: np.ndarray) -> float:
@@ -351,9 +403,8 @@ def run_reference(args, rank, world):
     only rank 0 runs; the other ranks exit without work."""
     if rank != 0:
         return 0
-    O = cpu_oracle(True)
-    model = O.OracleModel.load(MODEL_PATH, fast=True)
-    cores = int(O.lib(True).oracle_hardware_concurrency())
+    arm = CpuArm()
+    model, cores = arm.m, arm.cores
     box = model.aabb
     if args.workload == "c5":
         _, rays = c5_sample(box, args.rays or C5_RAYS)
@@ -375,7 +426,7 @@ def run_reference(args, rank, world):
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
         for r, mode in sets:
-            model.narrow_phase(r, mode, 0)
+            arm.run(r, mode)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -391,12 +442,9 @@ def run_reference(args, rank, world):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload], "rays_per_step": n,
                    "parallelism": "host threads (parallel_slices)"},
-        "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                              "sample": sample}, **ref_detail),
+        "cpu_baseline": dict({"value": value, "unit": UNIT, "cores": cores, "kind": arm.kind,
+                              "sample": sample, "what": arm.what}, **ref_detail),
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "reference cannot be built here (Eigen3/CLI11 absent); timed arm is the oracle's "
-                "C++ restatement of run_narrow_phase + infer_batch built with the reference's "
-                "flags (-O3 -march=native)",
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -923,21 +971,20 @@ def run_c5(args, ctx) -> None:
                                   clocks.get("sm_mhz"), pts / band, vol / band))
         if world == 1 and not args.no_cpu_baseline:
             try:
-                O = cpu_oracle(True)
-                om = O.OracleModel.load(MODEL_PATH, fast=True)
+                arm = CpuArm()
                 idx, srays = c5_sample(box, total)
-                rate, info = time_cpu_sets(om, [(srays, 0)], args.cpu_seconds)
-                cores = int(O.lib(True).oracle_hardware_concurrency())
+                rate, info = time_cpu_sets(arm, [(srays, 0)], args.cpu_seconds)
                 line["cpu_baseline"] = {
-                    "value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                    "value": rate, "unit": UNIT, "cores": arm.cores, "kind": arm.kind,
                     "sample": f"every {C5_CPU_STRIDE}th ray of the C5 frame ({info['rays']} rays, the "
                               f"reference arm's rays), best of {info['reps']} passes (~{info['seconds']:.1f} s "
-                              f"of CPU work)"}
-                line["cpu_baseline"].update(cpu_detail(rate, cores, pairs_fraction(om, srays), model.info.hidden,
-                                                       model.input_width, 8 + model.info.n_mat))
+                              f"of CPU work)", "what": arm.what}
+                line["cpu_baseline"].update(cpu_detail(rate, arm.cores, pairs_fraction(arm.m, srays),
+                                                       model.info.hidden, model.input_width, 8 + model.info.n_mat))
                 # the sample doubles as a parity spot check of the timed frame
+                # against the IEEE (parity) build of the same CPU path
                 gpu = lsnif.wire_to_hits(d_frame.cpu().numpy()[idx.astype(np.int64)])
-                line["sample_parity"] = sample_parity(gpu, om.narrow_phase(srays, 0, 0))
+                line["sample_parity"] = sample_parity(gpu, parity_model().narrow_phase(srays, 0, 0))
             except Exception as e:  # reported, never silently substituted
                 line["cpu_baseline"] = {"value": None, "error": str(e)}
         print(json.dumps(line), flush=True)
@@ -1041,21 +1088,19 @@ def run_single(args, ctx) -> None:
                                   clocks.get("sm_mhz"), pts / n_step, vol / n_step))
         if world == 1 and not args.no_cpu_baseline:
             try:
-                O = cpu_oracle(True)
-                om = O.OracleModel.load(MODEL_PATH, fast=True)
+                arm = CpuArm()
                 if args.workload == "c3":
                     sets = [(primary[::8], 0)]
                     smp = f"every 8th C3 ray ({len(sets[0][0])} rays)"
                 else:
                     sets = [(primary, 0), (shadow, 1)]
                     smp = f"the whole frame: {len(primary)} primary + {len(shadow)} shadow rays"
-                rate, info = time_cpu_sets(om, sets, args.cpu_seconds)
-                cores = int(O.lib(True).oracle_hardware_concurrency())
-                line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                rate, info = time_cpu_sets(arm, sets, args.cpu_seconds)
+                line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": arm.cores, "kind": arm.kind,
                                         "sample": f"{smp}, best of {info['reps']} passes "
-                                                  f"(~{info['seconds']:.1f} s of CPU work)"}
-                line["cpu_baseline"].update(cpu_detail(rate, cores,
-                                                       pairs_fraction(om, np.concatenate([r for r, _ in sets])),
+                                                  f"(~{info['seconds']:.1f} s of CPU work)", "what": arm.what}
+                line["cpu_baseline"].update(cpu_detail(rate, arm.cores,
+                                                       pairs_fraction(arm.m, np.concatenate([r for r, _ in sets])),
                                                        model.info.hidden, model.input_width, 8 + model.info.n_mat))
             except Exception as e:
                 line["cpu_baseline"] = {"value": None, "error": str(e)}

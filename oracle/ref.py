@@ -61,6 +61,8 @@ def lib(fast: bool = False) -> C.CDLL:
         L.ref_scene_query.argtypes = [_P, _P, C.c_int64, C.c_int, _P, C.c_int]
         L.ref_time_scene_query.restype = C.c_double
         L.ref_time_scene_query.argtypes = [_P, _P, C.c_int64, C.c_int, _P, C.c_int, C.c_int]
+        L.ref_build_obj_model.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_uint64]
+        L.ref_build_shape_model.argtypes = [C.c_int, C.c_uint64, C.c_char_p]
         _LIBS[fast] = L
     return _LIBS[fast]
 
@@ -139,6 +141,20 @@ class RefModel:
             self.L.ref_model_free(self.h)
         except Exception:
             pass
+
+
+def build_obj_model(obj_path: str, out_path: str, V: int = 32, H: int = 18, seed: int = 0) -> None:
+    """The reference's train() setup state (T = 0) for an OBJ mesh, saved as LSNF v1."""
+    L = lib(False)
+    if L.ref_build_obj_model(obj_path.encode(), out_path.encode(), V, H, seed) != 0:
+        raise RuntimeError(L.ref_last_error().decode())
+
+
+def build_shape_model(shape: int, seed: int, out_path: str) -> None:
+    """Same for a shapes.cpp fixture: 0 sphere, 1 box (1, .6, .8), 2 torus."""
+    L = lib(False)
+    if L.ref_build_shape_model(shape, seed, out_path.encode()) != 0:
+        raise RuntimeError(L.ref_last_error().decode())
 
 
 def hardware_concurrency(fast: bool = True) -> int:

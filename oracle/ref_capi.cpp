@@ -18,7 +18,11 @@
 #include "lsnif/model_io.hpp"
 #include "lsnif/parallel.hpp"
 #include "lsnif/renderer.hpp"
+#include "lsnif/obj.hpp"
 #include "lsnif/scene.hpp"
+#include "lsnif/shapes.hpp"
+#include "lsnif/training.hpp"
+#include "lsnif/voxel.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -356,6 +360,43 @@ double ref_time_scene_query(void* mp, const RayRec* rays, int64_t n, int mode, S
     }
   });
   return st < 0 ? st : best;
+}
+
+// The T = 0 state of train() (training.cpp:100-128: LocalFrame::for_mesh,
+// voxelize_surface, make_sparse_hash_grid, make_mlp with TrainConfig's
+// defaults and the given V, H, seed) saved with save_model — the reference
+// generating the test fixtures the oracle generated.
+static void save_setup_model(const lsnif::Mesh& mesh, int V, int H, uint64_t seed, const char* out) {
+  lsnif::TrainConfig cfg;
+  cfg.voxel_res = V;
+  cfg.hit_cap = H;
+  cfg.seed = seed;
+  const lsnif::LocalFrame frame = lsnif::LocalFrame::for_mesh(mesh);
+  lsnif::LsnifModel model;
+  model.voxel_res = cfg.voxel_res;
+  model.hit_cap = cfg.hit_cap;
+  model.occupancy = lsnif::voxelize_surface(mesh, frame, cfg.voxel_res);
+  model.grid = lsnif::make_sparse_hash_grid<lsnif::Real>(cfg.voxel_res, cfg.level_res, cfg.f_dim, cfg.table_size,
+                                                         cfg.seed);
+  const int input_width = cfg.hit_cap * model.grid.n_levels() * cfg.f_dim;
+  model.mlp = lsnif::make_mlp<lsnif::Real>(input_width, cfg.hidden_width, mesh.n_materials(), cfg.seed);
+  model.materials = mesh.materials;
+  model.aabb = frame.aabb;
+  lsnif::save_model(model, out);
+}
+
+int ref_build_obj_model(const char* obj_path, const char* out_path, int V, int H, uint64_t seed) {
+  return guarded([&] { save_setup_model(lsnif::load_obj(obj_path), V, H, seed, out_path); });
+}
+
+// shape: 0 make_uv_sphere(), 1 make_box((1, .6, .8)), 2 make_torus() (shapes.cpp)
+int ref_build_shape_model(int shape, uint64_t seed, const char* out_path) {
+  return guarded([&] {
+    lsnif::Mesh mesh = shape == 0   ? lsnif::make_uv_sphere()
+                       : shape == 1 ? lsnif::make_box(lsnif::Vec3(1.0f, 0.6f, 0.8f))
+                                    : lsnif::make_torus();
+    save_setup_model(mesh, 32, 18, seed, out_path);
+  });
 }
 
 }  // extern "C"

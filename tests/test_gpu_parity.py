@@ -16,6 +16,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from paper_2504_21627_b200 import lsnif, workloads as W  # noqa: E402
+from helpers import edge_rays  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -23,38 +24,6 @@ def gmodel(teapot_path):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return lsnif.GpuModel(teapot_path, 0)
-
-
-def edge_rays(box):
-    """Hand-built edge cases: inside origins, axis-aligned and grid-plane
-    origins, zero direction components, t_max gating, misses."""
-    mn, mx = box[:3], box[3:]
-    c = (mn + mx) / 2
-    rs = []
-    def add(o, d, t0=0.0, t1=np.inf):
-        rs.append((np.array(o, np.float32), np.array(d, np.float32), t0, t1))
-    add(c, (1, 0, 0)); add(c, (0, 1, 0)); add(c, (0, 0, -1))
-    add(mn - 1, (1, 1, 1) / np.sqrt(3)); add(mx + 1, -np.ones(3) / np.sqrt(3))
-    add((mn[0] - 1, c[1], c[2]), (1, 0, 0))           # axis aligned through the centre
-    add((mn[0] - 1, mn[1], mn[2]), (1, 0, 0))         # along a box edge
-    add((mn[0] - 1, c[1], c[2]), (-1, 0, 0))          # pointing away
-    add((mn[0] - 1, c[1], c[2]), (1, 0, 0), 0.0, 0.5)  # t_max before the box: no pair
-    add((mn[0] - 1, c[1], c[2]), (1, 0, 0), 2.0)       # t_min inside the box
-    add(mn, (0.3, 0.4, 0.5)); add(mx, (-0.3, -0.4, -0.5))
-    ext = mx - mn
-    for k in range(32):                                # origins exactly on grid planes
-        p = mn + ext * np.float32(k / 32)
-        add(p, (0.6, 0.64, 0.48))
-        add((p[0], c[1], c[2]), (0.0, 0.6, 0.8))
-    rng = np.random.default_rng(7)
-    for _ in range(200):                               # zero direction components
-        d = rng.standard_normal(3).astype(np.float32)
-        d[rng.integers(0, 3)] = 0.0
-        add(rng.uniform(mn - 0.5, mx + 0.5).astype(np.float32), d / np.linalg.norm(d))
-    out = np.zeros(len(rs), W.RAY_DTYPE)
-    for i, (o, d, t0, t1) in enumerate(rs):
-        out[i] = (o, d, t0, t1)
-    return out
 
 
 def workload_sets(box):
@@ -407,3 +376,40 @@ def test_query_rejects_bad_output_buffers(gmodel):
         gmodel.query_wire(d, out=torch.empty((256, 8), dtype=torch.int32, device="cuda"))
     with pytest.raises(ValueError):
         gmodel.query(d[:, :6])
+
+
+def test_gpu_against_reference_golden_vectors(gmodel):
+    """The GPU path against vectors written by the reference itself
+    (tests/golden/make_ref_vectors.py via oracle/_ref): traversal, hash
+    indices and features bit-exact; query within the App. B gates."""
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_teapot_vectors.npz"))
+    rays = np.ascontiguousarray(g["rays"]).view(W.RAY_DTYPE).reshape(-1)
+    got = {k: v.cpu().numpy() for k, v in gmodel.debug_traverse(lsnif.rays_to_tensor(rays)).items()}
+    assert np.array_equal(got["info"], g["info"])
+    for k in ("interval", "t", "pts", "feat"):
+        assert np.array_equal(got[k].view(np.uint32), g[k + "_bits"]), k
+    assert np.array_equal(got["cells"].view(np.uint32), g["cells"])
+    assert np.array_equal(got["hidx"].view(np.uint32), g["hidx"])
+    for mode, key in ((0, "hits_closest"), (1, "hits_any")):
+        ref = np.ascontiguousarray(g[key]).view(lsnif.HIT_DTYPE).reshape(-1)
+        hits = lsnif.hits_to_numpy(gmodel.query(lsnif.rays_to_tensor(rays), mode))
+        vis, mat, both, dt = compare_query(hits, ref, key)
+        assert vis >= 0.999 and mat >= 0.999
+
+
+def test_gpu_against_reference_library(gmodel, teapot_path):
+    """Directly against the reference's own narrow phase (oracle/_ref, built in
+    the build container; the library travels with the repo)."""
+    from oracle import ref as R
+    if not os.path.exists(R.LIBS[False]):
+        pytest.skip("oracle/_ref not built")
+    rm = R.RefModel(teapot_path)
+    rays = W.incoherent_rays(200_000, gmodel.aabb, seed=77)
+    ref = rm.narrow_phase(rays, 0, 0)
+    got = lsnif.hits_to_numpy(gmodel.query(lsnif.rays_to_tensor(rays)))
+    vis, mat, both, dt = compare_query(got, ref, "ref")
+    assert vis >= 0.999 and mat >= 0.999
+    tr = rm.trace(rays[:20000])
+    gt = {k: v.cpu().numpy() for k, v in gmodel.debug_traverse(lsnif.rays_to_tensor(rays[:20000])).items()}
+    assert np.array_equal(gt["hidx"].view(np.uint32), tr["hidx"])
+    assert np.array_equal(gt["feat"].view(np.uint32), tr["feat"].view(np.uint32))

@@ -305,3 +305,25 @@ def test_teapot_fixture_statistics(oracle_teapot):
     cnt, pair = tr["info"] & 255, (tr["info"] >> 9) & 1
     assert abs(pair.mean() - 0.656) < 0.01
     assert abs(cnt[pair == 1].mean() - 3.64) < 0.15
+
+
+def test_oracle_reproduces_reference_golden_vectors(oracle_teapot):
+    """The golden vectors written by the reference itself
+    (tests/golden/make_ref_vectors.py, oracle/_ref) pin the restatement even
+    where /root/reference is absent: DDA / hash / features and both
+    narrow-phase accept rules, bit for bit."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_teapot_vectors.npz"))
+    rays = np.ascontiguousarray(g["rays"]).view(oracle_teapot_ray_dtype()).reshape(-1)
+    tr = oracle_teapot.trace(rays)
+    assert np.array_equal(tr["info"], g["info"])
+    for k in ("interval", "t", "pts", "feat"):
+        assert np.array_equal(np.asarray(tr[k]).view(np.uint32), g[k + "_bits"]), k
+    assert np.array_equal(tr["cells"], g["cells"]) and np.array_equal(tr["hidx"], g["hidx"])
+    assert oracle_teapot.narrow_phase(rays, 0, 1).view(np.uint32).tobytes() == g["hits_closest"].tobytes()
+    assert oracle_teapot.narrow_phase(rays, 1, 1).view(np.uint32).tobytes() == g["hits_any"].tobytes()
+
+
+def oracle_teapot_ray_dtype():
+    from oracle import oracle as O
+    return O.RAY_DTYPE
