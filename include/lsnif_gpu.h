@@ -126,6 +126,7 @@ typedef struct lsnif_model_info {
   float aabb[6];
   float activation_scale; /* power-of-two fp16 operand scale */
   uint64_t device_bytes;
+  int32_t device; /* CUDA device ordinal the model lives on */
 } lsnif_model_info;
 
 /* Counters of the last lsnif_query on a stream (filled when requested). */

@@ -92,6 +92,29 @@ class Model {
   std::shared_ptr<lsnif_model_s> h_;
 };
 
+// The model's device made current for the adapter's own allocations and
+// copies, the caller's current device restored on exit (RAII).
+class DeviceScope {
+ public:
+  explicit DeviceScope(const Model& model) : DeviceScope(model.info().device) {}
+  explicit DeviceScope(int device) {  // device < 0: stay on the current device
+    if (device < 0) return;
+    if (cudaGetDevice(&prev_) != cudaSuccess) prev_ = -1;
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  }
+  ~DeviceScope() {
+    if (prev_ >= 0) cudaSetDevice(prev_);
+  }
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+  static void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+
+ private:
+  int prev_ = -1;
+};
+
 // Device buffer helper (RAII).
 template <typename T>
 struct DeviceBuffer {
@@ -112,16 +135,23 @@ inline std::vector<NeuralHit> infer_batch(const Model& model, const std::vector<
   const int64_t n = rows ? static_cast<int64_t>(inputs.size()) / rows : 0;
   if (n * rows != static_cast<int64_t>(inputs.size()))
     throw std::invalid_argument("infer_batch: input width mismatch");
+  DeviceScope on(model);
   DeviceBuffer<float> dx(inputs.size());
   DeviceBuffer<lsnif_interval> di(intervals.size());
   DeviceBuffer<lsnif_hit> dh(static_cast<size_t>(n));
-  if (!inputs.empty()) cudaMemcpy(dx.ptr, inputs.data(), inputs.size() * 4, cudaMemcpyHostToDevice);
+  if (!inputs.empty())
+    DeviceScope::cuda_check(cudaMemcpy(dx.ptr, inputs.data(), inputs.size() * 4, cudaMemcpyHostToDevice),
+                            "cudaMemcpy(inputs)");
   if (!intervals.empty())
-    cudaMemcpy(di.ptr, intervals.data(), intervals.size() * sizeof(lsnif_interval), cudaMemcpyHostToDevice);
+    DeviceScope::cuda_check(cudaMemcpy(di.ptr, intervals.data(), intervals.size() * sizeof(lsnif_interval),
+                                       cudaMemcpyHostToDevice),
+                            "cudaMemcpy(intervals)");
   check(lsnif_infer_batch(model.handle(), dx.ptr, rows, n, di.ptr, static_cast<int64_t>(intervals.size()),
                           dh.ptr, nullptr));
   std::vector<lsnif_hit> raw(static_cast<size_t>(n));
-  if (n) cudaMemcpy(raw.data(), dh.ptr, raw.size() * sizeof(lsnif_hit), cudaMemcpyDeviceToHost);
+  if (n)
+    DeviceScope::cuda_check(cudaMemcpy(raw.data(), dh.ptr, raw.size() * sizeof(lsnif_hit), cudaMemcpyDeviceToHost),
+                            "cudaMemcpy(hits)");
   std::vector<NeuralHit> out;
   out.reserve(raw.size());
   for (const lsnif_hit& h : raw) out.push_back(to_neural_hit(h));
@@ -145,16 +175,21 @@ inline std::vector<NeuralHit> infer_pairs(const Model& model, const std::vector<
                                           int mode = LSNIF_QUERY_CLOSEST) {
   if (rays.size() != pairs.size()) throw std::invalid_argument("infer_pairs: one interval per ray");
   const size_t n = rays.size();
+  DeviceScope on(model);
   DeviceBuffer<lsnif_ray> dr(n);
   DeviceBuffer<lsnif_interval> di(n);
   DeviceBuffer<lsnif_hit> dh(n);
   if (n) {
-    cudaMemcpy(dr.ptr, rays.data(), n * sizeof(lsnif_ray), cudaMemcpyHostToDevice);
-    cudaMemcpy(di.ptr, pairs.data(), n * sizeof(lsnif_interval), cudaMemcpyHostToDevice);
+    DeviceScope::cuda_check(cudaMemcpy(dr.ptr, rays.data(), n * sizeof(lsnif_ray), cudaMemcpyHostToDevice),
+                            "cudaMemcpy(rays)");
+    DeviceScope::cuda_check(cudaMemcpy(di.ptr, pairs.data(), n * sizeof(lsnif_interval), cudaMemcpyHostToDevice),
+                            "cudaMemcpy(pairs)");
   }
   check(lsnif_query_pairs(model.handle(), dr.ptr, di.ptr, static_cast<int64_t>(n), mode, dh.ptr, nullptr));
   std::vector<lsnif_hit> raw(n);
-  if (n) cudaMemcpy(raw.data(), dh.ptr, n * sizeof(lsnif_hit), cudaMemcpyDeviceToHost);
+  if (n)
+    DeviceScope::cuda_check(cudaMemcpy(raw.data(), dh.ptr, n * sizeof(lsnif_hit), cudaMemcpyDeviceToHost),
+                            "cudaMemcpy(hits)");
   std::vector<NeuralHit> out;
   out.reserve(n);
   for (const lsnif_hit& h : raw) out.push_back(to_neural_hit(h));
@@ -197,6 +232,7 @@ class Scene {
   }
   lsnif_scene handle() const { return h_.get(); }
   size_t size() const { return models_.size(); }
+  int device() const { return models_.empty() ? -1 : models_.front().info().device; }
 
   // intersect_scene (renderer.cpp:269-303) / occluded_batch (305-323) for a
   // scene without triangle objects; WORLD-space host rays.
@@ -233,12 +269,15 @@ inline std::vector<float> render(const Scene& scene, const std::vector<float>& w
                                  lsnif_render_stats* stats = nullptr) {
   const size_t px = static_cast<size_t>(config.width > 0 ? config.width : 0) *
                     static_cast<size_t>(config.height > 0 ? config.height : 0);
+  DeviceScope on(scene.device());
   DeviceBuffer<float> img(3 * px);
   check(lsnif_render(scene.handle(), world_diag.data(), static_cast<int32_t>(world_diag.size()), &camera,
                      lights.data(), static_cast<int32_t>(lights.size()), environment, &config, img.ptr, stats,
                      nullptr));
   std::vector<float> out(3 * px);
-  if (px) cudaMemcpy(out.data(), img.ptr, out.size() * sizeof(float), cudaMemcpyDeviceToHost);
+  if (px)
+    DeviceScope::cuda_check(cudaMemcpy(out.data(), img.ptr, out.size() * sizeof(float), cudaMemcpyDeviceToHost),
+                            "cudaMemcpy(image)");
   return out;
 }
 

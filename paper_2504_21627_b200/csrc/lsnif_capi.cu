@@ -29,8 +29,21 @@ using lsnif_api::ApiError;
 using lsnif_api::ck;
 using lsnif_api::fail;
 
+// Every entry point restores the caller's current device on return (the
+// body switches to the model's / scene's device).
+struct DeviceRestore {
+  int dev = -1;
+  DeviceRestore() {
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+  }
+  ~DeviceRestore() {
+    if (dev >= 0) cudaSetDevice(dev);
+  }
+};
+
 template <typename F>
 lsnif_status guarded(F&& f) {
+  DeviceRestore restore;
   try {
     f();
     return LSNIF_OK;
@@ -501,6 +514,7 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
     m.zero_flags = zh.flags_material & ~static_cast<uint32_t>(LSNIF_HIT_PAIR | LSNIF_HIT_ACCEPTED);
   }
 
+  M.info.device = M.device;
   M.info.voxel_res = V;
   M.info.hit_cap = H;
   M.info.n_levels = L;

@@ -524,6 +524,59 @@ __device__ __forceinline__ void decode_albedo(float z5, float z6, float z7, floa
   albedo[2] = sigmoid_ref(z7);
 }
 
+// Reduced-instruction decode for the MLP epilogue (the outputs the parity
+// contract takes within a tolerance: t_world, normal, albedo; SURVEY.md
+// App. B): sigmoid from the hardware exp2 / reciprocal (a few ulp), the
+// normal scaled by a hardware reciprocal square root, and the material as
+// the first maximum of the logits (softmax is monotone: the same index as
+// the reference's first maximum of the probabilities unless two logits
+// round to the same probability). The visibility decision is unchanged
+// (z0 >= occ_threshold).
+__device__ __forceinline__ float sigmoid_fast(float v) {
+  return __frcp_rn(__fadd_rn(1.0f, exp2f(__fmul_rn(v, -1.4426950408889634f))));
+}
+
+__device__ __forceinline__ void decode_flags_fast(float z0, float z1, const float* zm, int n_mat,
+                                                  float occ_threshold, float enter, float exit, float t_min,
+                                                  float t_max, int mode, uint32_t& flags_material,
+                                                  float& t_world) {
+  const float lt = sigmoid_fast(z1);
+  const bool occluded = z0 >= occ_threshold;
+  const float tw = __fadd_rn(enter, __fmul_rn(lt, __fsub_rn(exit, enter)));
+  constexpr int kMaxMat = 8;
+  int arg = 0;
+  float best = zm[0];
+#pragma unroll
+  for (int k = 1; k < kMaxMat; ++k)
+    if (k < n_mat && zm[k] > best) {
+      best = zm[k];
+      arg = k;
+    }
+  uint32_t flags = LSNIF_HIT_PAIR;
+  if (occluded) {
+    flags |= LSNIF_HIT_OCCLUDED;
+    const bool accept = (mode == LSNIF_QUERY_CLOSEST) ? !(tw >= t_max || tw < t_min)
+                                                      : (tw >= t_min && tw <= t_max);
+    if (accept) flags |= LSNIF_HIT_ACCEPTED;
+  }
+  flags_material = flags | (static_cast<uint32_t>(arg) << LSNIF_HIT_MATERIAL_SHIFT);
+  t_world = tw;
+}
+
+__device__ __forceinline__ void decode_normal_fast(float n0, float n1, float n2, float normal[3]) {
+  const float len2 = __fadd_rn(__fadd_rn(__fmul_rn(n0, n0), __fmul_rn(n1, n1)), __fmul_rn(n2, n2));
+  const float inv = len2 > 1e-24f ? rsqrtf(len2) : 0.0f;
+  normal[0] = __fmul_rn(n0, inv);
+  normal[1] = __fmul_rn(n1, inv);
+  normal[2] = __fmul_rn(n2, inv);
+}
+
+__device__ __forceinline__ void decode_albedo_fast(float z5, float z6, float z7, float albedo[3]) {
+  albedo[0] = sigmoid_fast(z5);
+  albedo[1] = sigmoid_fast(z6);
+  albedo[2] = sigmoid_fast(z7);
+}
+
 __device__ __forceinline__ void decode_hit(const float* z, int n_mat, float occ_threshold,
                                            float enter, float exit, float t_min, float t_max,
                                            int mode, bool pair_flag, lsnif_hit& h) {

@@ -410,17 +410,15 @@ struct MlpLayout {
   static constexpr uint32_t kACol = HID;      // A_h column offset within a group
 };
 
-// leaky_relu(v, 0.01) (mlp.hpp:80-94) as 0.505 v + 0.495 |v|: an FMUL and an
-// FFMA, both immediate forms on the FMA pipe, instead of FMUL + FMNMX (the
-// ALU pipe, which the epilogue saturates). The fp32 constants sum to exactly
-// 1 (slope 1 for v >= 0, within 1 ulp of v) and differ by 0.01 (1 - 9.5e-7)
-// for v < 0; the result is rounded to fp16 right after, so the difference to
-// fmaxf(v, 0.01 v) is below the fp16 rounding of the activations.
-__device__ __forceinline__ float leaky_fma(float v) {
-  return __fmaf_rn(fabsf(v), 0.495f, __fmul_rn(v, 0.505f));
-}
+// leaky_relu(v, 0.01) (mlp.hpp:80-94) on a packed pair: the fp32 accumulator
+// pair is rounded to fp16 once (F2FP), then max(h, 0.01 h) in half2 (HFMA2 +
+// HMNMX2): 1.5 instructions per activation instead of 2.5 for the fp32 form
+// (the epilogue is issue-bound). Non-negative activations are exactly their
+// fp16 rounding, as before; negative ones are 0.01 (as fp16) times the
+// rounded value, rounded (a second rounding on the 1%-slope side only).
 __device__ __forceinline__ uint32_t leaky_pack(uint32_t a, uint32_t b) {
-  const __half2 h = __floats2half2_rn(leaky_fma(__uint_as_float(a)), leaky_fma(__uint_as_float(b)));
+  const __half2 v = __floats2half2_rn(__uint_as_float(a), __uint_as_float(b));
+  const __half2 h = __hmax2(v, __hmul2(v, __float2half2_rn(0.01f)));
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
@@ -721,12 +719,12 @@ __global__ void __launch_bounds__(MlpLayout<HID>::kThreads, 1) mlp_tc_kernel(con
         for (int k = 0; k < 8; ++k) zm[k] = k < m.n_mat ? zs[(2 + k) * 32] : 0.0f;
         uint32_t fm;
         float tw;
-        decode_flags(zs[0], zs[32], zm, m.n_mat, m.occ_threshold, pa.y, pa.z, pa.w, pb.x, P.mode, true, fm, tw);
+        decode_flags_fast(zs[0], zs[32], zm, m.n_mat, m.occ_threshold, pa.y, pa.z, pa.w, pb.x, P.mode, fm, tw);
         *reinterpret_cast<float2*>(dst) = make_float2(__uint_as_float(fm), tw);
       } else {
         float nrm[3], alb[3];
-        decode_normal(zs[0], zs[32], zs[64], nrm);
-        decode_albedo(zs[96], zs[128], zs[160], alb);
+        decode_normal_fast(zs[0], zs[32], zs[64], nrm);
+        decode_albedo_fast(zs[96], zs[128], zs[160], alb);
         if (P.wire) {
           uint32_t no, al;
           wire_pack_normal_albedo(nrm, alb, no, al);

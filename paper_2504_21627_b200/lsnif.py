@@ -48,7 +48,7 @@ class ModelInfo(C.Structure):
                 ("f_dim", C.c_int32), ("table_size", C.c_uint32), ("hidden", C.c_int32),
                 ("n_mat", C.c_int32), ("n_materials", C.c_int32), ("level_res", C.c_int32 * 4),
                 ("aabb", C.c_float * 6), ("activation_scale", C.c_float),
-                ("device_bytes", C.c_uint64)]
+                ("device_bytes", C.c_uint64), ("device", C.c_int32)]
 
 
 class Profile(C.Structure):
