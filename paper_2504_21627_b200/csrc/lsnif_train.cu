@@ -19,7 +19,6 @@
 //   adam_kernel      adam_update_tensor (mlp.hpp:243-256) over MLP and tables.
 // Random numbers come from per-sample counter streams (splitmix64), not the
 // reference's per-worker mt19937 stream, whose retry loops make it serial.
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -583,9 +582,9 @@ __global__ void adam_kernel(float* param, const float* grad, float* m, float* v,
 
 namespace lsnif_tr {
 
-void cublas_ck(cublasStatus_t s, const char* what) {
-  if (s != CUBLAS_STATUS_SUCCESS) fail(LSNIF_CUDA_ERROR, std::string(what) + ": cuBLAS status " + std::to_string(s));
-}
+// tcgen05 split-TF32 GEMM (lsnif_tcgemm.cu), cublasSgemm semantics
+cudaError_t tcgemm_colmajor(bool ta, bool tb, int mm, int nn, int kk, const float* A, int lda, const float* B, int ldb,
+                            float* C, int ldc, float* work, size_t work_floats, int num_sms, cudaStream_t st);
 
 struct Trainer {
   int device = 0;
@@ -603,7 +602,9 @@ struct Trainer {
   Frame frame{};
   lsnif_train_config cfg{};
   int64_t step = 0;
-  cublasHandle_t blas = nullptr;
+  int num_sms = 148;
+  float* gemm_work = nullptr;  // split-K partials of the batch reductions
+  size_t gemm_work_floats = 0;
   std::vector<void*> allocs;
   // batch buffers
   int64_t cap = 0;
@@ -655,7 +656,6 @@ struct Trainer {
     cudaFree(grads);
     cudaFree(m);
     cudaFree(v);
-    if (blas) cublasDestroy(blas);
     if (geo) lsnif_model_destroy(geo);
   }
 };
@@ -667,16 +667,17 @@ void launch(K kern, int64_t n, int threads, size_t smem, cudaStream_t st, const 
   ck(cudaGetLastError(), what);
 }
 
-void gemm(Trainer& T, cublasOperation_t ta, cublasOperation_t tb, int mm, int nn, int kk, const float* A, int lda,
+constexpr bool OP_N = false, OP_T = true;
+
+void gemm(Trainer& T, cudaStream_t st, bool ta, bool tb, int mm, int nn, int kk, const float* A, int lda,
           const float* B, int ldb, float* Cm, int ldc) {
-  const float one = 1.0f, zero = 0.0f;
-  cublas_ck(cublasSgemm(T.blas, ta, tb, mm, nn, kk, &one, A, lda, B, ldb, &zero, Cm, ldc), "cublasSgemm");
+  ck(tcgemm_colmajor(ta, tb, mm, nn, kk, A, lda, B, ldb, Cm, ldc, T.gemm_work, T.gemm_work_floats, T.num_sms, st),
+     "tcgemm_kernel");
 }
 
 // Forward + loss + backward of one batch into T.grads (zeroed first) and T.loss6.
 void batch_grads(Trainer& T, const lsnif_ray* rays, const lsnif_train_target* tg, int64_t n, cudaStream_t st) {
   T.ensure_batch(n);
-  cublas_ck(cublasSetStream(T.blas, st), "cublasSetStream");
   ck(cudaMemsetAsync(T.grads, 0, T.n_params * sizeof(float), st), "cudaMemsetAsync");
   ck(cudaMemsetAsync(T.loss6, 0, 8 * sizeof(float), st), "cudaMemsetAsync");
   const int nn = static_cast<int>(n);
@@ -685,27 +686,27 @@ void batch_grads(Trainer& T, const lsnif_ray* rays, const lsnif_train_target* tg
   launch(encode_kernel, n, 128, static_cast<size_t>(T.dm.stop_words) * 4, st, "encode_kernel", T.dm, P, rays, n, T.X,
          T.cidx, T.cw, T.ccount);
   // forward_cached (mlp.hpp:117-130); weights row-major [out][in] = col-major [in][out]
-  gemm(T, CUBLAS_OP_T, CUBLAS_OP_N, T.hid, nn, T.K1, P + T.off_w1, T.K1, T.X, T.K1, T.z1, T.hid);
+  gemm(T, st, OP_T, OP_N, T.hid, nn, T.K1, P + T.off_w1, T.K1, T.X, T.K1, T.z1, T.hid);
   launch(bias_leaky_kernel, static_cast<int64_t>(T.hid) * n, 256, 0, st, "bias_leaky", T.z1, T.h1, P + T.off_b1, T.hid, n);
-  gemm(T, CUBLAS_OP_T, CUBLAS_OP_N, T.hid, nn, T.hid, P + T.off_w2, T.hid, T.h1, T.hid, T.z2, T.hid);
+  gemm(T, st, OP_T, OP_N, T.hid, nn, T.hid, P + T.off_w2, T.hid, T.h1, T.hid, T.z2, T.hid);
   launch(bias_leaky_kernel, static_cast<int64_t>(T.hid) * n, 256, 0, st, "bias_leaky", T.z2, T.h2, P + T.off_b2, T.hid, n);
-  gemm(T, CUBLAS_OP_T, CUBLAS_OP_N, T.n_out, nn, T.hid, P + T.off_w3, T.hid, T.h2, T.hid, T.z3, T.n_out);
+  gemm(T, st, OP_T, OP_N, T.n_out, nn, T.hid, P + T.off_w3, T.hid, T.h2, T.hid, T.z3, T.n_out);
   launch(heads_loss_kernel, n, 128, 0, st, "heads_loss_kernel", static_cast<const float*>(T.z3), P + T.off_b3, T.n_out,
          T.n_mat, n, tg, 1.0f / static_cast<float>(n), T.dz3, T.loss6);
   // backward (mlp.hpp:206-225)
-  gemm(T, CUBLAS_OP_N, CUBLAS_OP_T, T.hid, T.n_out, nn, T.h2, T.hid, T.dz3, T.n_out, G + T.off_w3, T.hid);
+  gemm(T, st, OP_N, OP_T, T.hid, T.n_out, nn, T.h2, T.hid, T.dz3, T.n_out, G + T.off_w3, T.hid);
   rowsum_kernel<<<T.n_out, 256, 0, st>>>(T.dz3, T.n_out, n, G + T.off_b3);
-  gemm(T, CUBLAS_OP_N, CUBLAS_OP_N, T.hid, nn, T.n_out, P + T.off_w3, T.hid, T.dz3, T.n_out, T.dh2, T.hid);
+  gemm(T, st, OP_N, OP_N, T.hid, nn, T.n_out, P + T.off_w3, T.hid, T.dz3, T.n_out, T.dh2, T.hid);
   launch(leaky_back_kernel, static_cast<int64_t>(T.hid) * n, 256, 0, st, "leaky_back", T.dh2, T.z2, T.dz2,
          static_cast<int64_t>(T.hid) * n);
-  gemm(T, CUBLAS_OP_N, CUBLAS_OP_T, T.hid, T.hid, nn, T.h1, T.hid, T.dz2, T.hid, G + T.off_w2, T.hid);
+  gemm(T, st, OP_N, OP_T, T.hid, T.hid, nn, T.h1, T.hid, T.dz2, T.hid, G + T.off_w2, T.hid);
   rowsum_kernel<<<T.hid, 256, 0, st>>>(T.dz2, T.hid, n, G + T.off_b2);
-  gemm(T, CUBLAS_OP_N, CUBLAS_OP_N, T.hid, nn, T.hid, P + T.off_w2, T.hid, T.dz2, T.hid, T.dh1, T.hid);
+  gemm(T, st, OP_N, OP_N, T.hid, nn, T.hid, P + T.off_w2, T.hid, T.dz2, T.hid, T.dh1, T.hid);
   launch(leaky_back_kernel, static_cast<int64_t>(T.hid) * n, 256, 0, st, "leaky_back", T.dh1, T.z1, T.dz1,
          static_cast<int64_t>(T.hid) * n);
-  gemm(T, CUBLAS_OP_N, CUBLAS_OP_T, T.K1, T.hid, nn, T.X, T.K1, T.dz1, T.hid, G + T.off_w1, T.K1);
+  gemm(T, st, OP_N, OP_T, T.K1, T.hid, nn, T.X, T.K1, T.dz1, T.hid, G + T.off_w1, T.K1);
   rowsum_kernel<<<T.hid, 256, 0, st>>>(T.dz1, T.hid, n, G + T.off_b1);
-  gemm(T, CUBLAS_OP_N, CUBLAS_OP_N, T.K1, nn, T.hid, P + T.off_w1, T.K1, T.dz1, T.hid, T.dx, T.K1);
+  gemm(T, st, OP_N, OP_N, T.K1, nn, T.hid, P + T.off_w1, T.K1, T.dz1, T.hid, T.dx, T.K1);
   ck(cudaGetLastError(), "rowsum_kernel");
   // hash-grid gradient (encoding.hpp:193-209)
   launch(scatter_kernel, n * T.H * T.L, 256, 0, st, "scatter_kernel", static_cast<const float*>(T.dx),
@@ -838,7 +839,9 @@ void* trainer_create(const lsnif_model_desc& d, const lsnif_mesh_desc& mesh, con
   const float diag = std::sqrt((ext[0] * ext[0] + ext[1] * ext[1]) + ext[2] * ext[2]);  // Aabb::diagonal
   fr.radius = 0.5f * diag;
   fr.eps = 1e-4f * diag;  // self_intersection_eps (training.cpp:15-17)
-  lsnif_tr::cublas_ck(cublasCreate(&T->blas), "cublasCreate");
+  ck(cudaDeviceGetAttribute(&T->num_sms, cudaDevAttrMultiProcessorCount, device), "cudaDeviceGetAttribute");
+  T->gemm_work_floats = static_cast<size_t>(T->num_sms) * 128 * 128;
+  T->gemm_work = T->dalloc<float>(T->gemm_work_floats, T->allocs);
   return T.release();
 }
 
