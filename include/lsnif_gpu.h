@@ -191,10 +191,19 @@ lsnif_status lsnif_hits_from_wire(const lsnif_hit_wire* h_wire, int64_t n, lsnif
  * MatX inputs(input_width, n) column-major fp32 (DEVICE), intervals n
  * entries (DEVICE). Throws-equivalent LSNIF_INVALID_ARGUMENT when
  * n != n_intervals or rows != input_width. Results carry OCCLUDED and the
- * NeuralHit fields; PAIR/ACCEPTED are not set. */
+ * NeuralHit fields; PAIR/ACCEPTED are not set. Runs the columns through the
+ * tcgen05 MLP (fp16 operands, the query path's numerics); columns with an
+ * input beyond the model's encoder range (|x| > max |table entry|) are
+ * answered by the fp32 kernel instead (decided on the device). Asynchronous
+ * on `stream`. */
 lsnif_status lsnif_infer_batch(lsnif_model model, const float* d_inputs, int64_t rows, int64_t n,
                                const lsnif_interval* d_intervals, int64_t n_intervals,
                                lsnif_hit* d_hits, void* stream);
+/* The same with fp32 CUDA-core arithmetic in the reference's summation order
+ * (mlp.hpp:121-130): a validation mode, ~100x slower. */
+lsnif_status lsnif_infer_batch_f32(lsnif_model model, const float* d_inputs, int64_t rows, int64_t n,
+                                   const lsnif_interval* d_intervals, int64_t n_intervals,
+                                   lsnif_hit* d_hits, void* stream);
 
 /* Bit-exactness probe: per-ray pair/interval, DDA boundary points, t
  * values, cells, hash indices and fp32 features, produced by the same device

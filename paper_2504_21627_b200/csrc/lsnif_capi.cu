@@ -403,6 +403,7 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
   e = std::max(-14, std::min(15, e));
   m.act_scale = std::ldexp(1.0f, e);
   m.inv_act_scale = std::ldexp(1.0f, -e);
+  m.feat_bound = xmax;
   M.info.activation_scale = m.act_scale;
 
   // UMMA canonical fp16 operands with the bias folded in as column K:
@@ -1130,6 +1131,51 @@ lsnif_status lsnif_hits_from_wire(const lsnif_hit_wire* h_wire, int64_t n, lsnif
 lsnif_status lsnif_infer_batch(lsnif_model model, const float* d_inputs, int64_t rows, int64_t n,
                                const lsnif_interval* d_intervals, int64_t n_intervals,
                                lsnif_hit* d_hits, void* stream) {
+  return guarded([&] {
+    check_model(model);
+    if (n != n_intervals) fail(LSNIF_INVALID_ARGUMENT, "infer_batch: inputs/intervals size mismatch");
+    if (rows != model->dm.K1) fail(LSNIF_INVALID_ARGUMENT, "infer_batch: input width mismatch");
+    if (n > 0 && (!d_inputs || !d_intervals || !d_hits)) fail(LSNIF_INVALID_ARGUMENT, "null pointer");
+    ck(cudaSetDevice(model->device), "cudaSetDevice");
+    if (n == 0) return;
+    // the caller's columns through the tcgen05 MLP (chunks of kChunk rows);
+    // a chunk with an input beyond the scale's operand bound is answered
+    // again by the fp32 kernel (device-side flag, no host round trip)
+    lsnif_model_s& M = *model;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Workspace& w = M.workspace(st, n);
+    const int64_t nchunks = (n + kChunk - 1) / kChunk;
+    if (static_cast<size_t>(nchunks) > kMaxChunks) fail(LSNIF_INVALID_ARGUMENT, "too many columns in one call");
+    ck(cudaMemsetAsync(w.counters, 0, kChunkCounterBytes * nchunks, st), "cudaMemsetAsync");
+    for (int64_t s = 0, ci = 0; s < n; s += kChunk, ++ci) {
+      const int64_t cn = std::min(kChunk, n - s);
+      uint8_t* cc = w.counters + kChunkCounterBytes * ci;
+      int32_t* rows = reinterpret_cast<int32_t*>(cc + 8);
+      int* overflow = reinterpret_cast<int*>(cc + 8 + 4 * lsnif_dev::kMaxBins);
+      ck(lsnif_dev::launch_infer_pack(M.dm, d_inputs + s * M.dm.K1, cn, d_intervals + s, w.X, w.meta, rows,
+                                      static_cast<int64_t>(w.x_tiles), overflow, st),
+         "infer_pack_kernel");
+      lsnif_dev::MlpParams mp{};
+      mp.m = M.dm;
+      mp.X = w.X;
+      mp.meta = w.meta;
+      mp.row_counter = rows;
+      mp.cap_tiles = static_cast<int64_t>(w.x_tiles);
+      mp.out = d_hits + s;
+      mp.wire = 0;
+      mp.mode = lsnif_dev::kInferMode;
+      ck(lsnif_dev::launch_mlp(mp, static_cast<int>((cn + kTileM - 1) / kTileM) + M.dm.n_bins, M.num_sms, st),
+         "mlp_tc_kernel");
+      ck(lsnif_dev::launch_infer_f32(M.dm, d_inputs + s * M.dm.K1, cn, d_intervals + s, d_hits + s, st,
+                                     overflow),
+         "infer_f32_kernel");
+    }
+  });
+}
+
+lsnif_status lsnif_infer_batch_f32(lsnif_model model, const float* d_inputs, int64_t rows, int64_t n,
+                                   const lsnif_interval* d_intervals, int64_t n_intervals, lsnif_hit* d_hits,
+                                   void* stream) {
   return guarded([&] {
     check_model(model);
     if (n != n_intervals) fail(LSNIF_INVALID_ARGUMENT, "infer_batch: inputs/intervals size mismatch");

@@ -19,6 +19,7 @@
 namespace lsnif_dev {
 
 constexpr int kMaxLevels = 4;
+constexpr int kInferMode = 2;  // MLP decode mode of lsnif_infer_batch (internal)
 constexpr int kMaxHitCap = 32;
 constexpr int kTileM = 128;  // rays per MMA tile (TMEM lanes)
 // MLP rows are binned by their used input width: bin b holds the rows whose
@@ -55,6 +56,7 @@ struct DevModel {
   uint32_t w1_bytes, w2_bytes, w3_bytes;
   const float* w_f32;                  // w1 | b1 | w2 | b2 | w3 | b3 (decoded fp32, row-major)
   float act_scale, inv_act_scale;      // power of two
+  float feat_bound;                    // max |feature| the scale was derived for (max |table entry|)
   float occ_threshold;                 // smallest z with 1/(1+expf(-z)) > 0.5 under the host libm
   const lsnif_material* materials;     // material table (model_io.cpp:159-164)
   int n_materials;
@@ -552,12 +554,13 @@ __device__ __forceinline__ void decode_flags_fast(float z0, float z1, const floa
       best = zm[k];
       arg = k;
     }
-  uint32_t flags = LSNIF_HIT_PAIR;
+  // kInferMode (lsnif_infer_batch): a bare NeuralHit, no pair / accept flags
+  uint32_t flags = mode == kInferMode ? 0u : LSNIF_HIT_PAIR;
   if (occluded) {
     flags |= LSNIF_HIT_OCCLUDED;
     const bool accept = (mode == LSNIF_QUERY_CLOSEST) ? !(tw >= t_max || tw < t_min)
                                                       : (tw >= t_min && tw <= t_max);
-    if (accept) flags |= LSNIF_HIT_ACCEPTED;
+    if (accept && mode != kInferMode) flags |= LSNIF_HIT_ACCEPTED;
   }
   flags_material = flags | (static_cast<uint32_t>(arg) << LSNIF_HIT_MATERIAL_SHIFT);
   t_world = tw;

@@ -111,8 +111,11 @@ size_t mlp_smem_bytes(const DevModel& m, int x_stages);
 int mlp_x_stages(const DevModel& m, size_t smem_limit);
 cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st);
 cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st);
+cudaError_t launch_infer_pack(const DevModel& m, const float* x, int64_t n, const lsnif_interval* iv, uint8_t* X,
+                              RowMeta* meta, int32_t* row_counter, int64_t cap_tiles, int* overflow,
+                              cudaStream_t st);
 cudaError_t launch_infer_f32(const DevModel& m, const float* x, int64_t n, const lsnif_interval* iv,
-                             lsnif_hit* out, cudaStream_t st);
+                             lsnif_hit* out, cudaStream_t st, const int* only_if = nullptr);
 
 }  // namespace lsnif_dev
 

@@ -1154,9 +1154,52 @@ cudaError_t launch_merge(const DevModel& m, const InstanceParams& ip, const lsni
 
 // One thread per column; exact fp32, sequential sum over the input index
 // (the oracle's order), unfused multiply-add.
+// lsnif_infer_batch on the tcgen05 MLP: the caller's encoded columns (column
+// j = inputs[j * K1 .. + K1), the reference's MatX inputs(K1, n)) become rows
+// of the top K bin's X tiles (fp16, times the activation scale, zero past
+// K1) with row metadata {j, enter, exit}; the bin's row count is set so
+// mlp_tc_kernel answers exactly these rows. An input beyond the bound the
+// scale was derived for (|x| > feat_bound: not an encoder output) raises
+// *overflow, which hands the whole call to the fp32 kernel below.
+__global__ void __launch_bounds__(256) infer_pack_kernel(const DevModel m, const float* __restrict__ x, int64_t n,
+                                                         const lsnif_interval* __restrict__ iv, uint8_t* X,
+                                                         RowMeta* meta, int32_t* row_counter, int64_t cap_tiles,
+                                                         int* overflow) {
+  const int top = m.n_bins - 1;
+  const int groups = m.K1P / 8;  // 16-byte column groups of a row
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t == 0) row_counter[top] = static_cast<int32_t>(n);
+  if (t >= n * groups) return;
+  const int64_t j = t / groups;
+  const int c0 = static_cast<int>(t - j * groups) * 8;
+  const float* xc = x + j * m.K1;
+  uint32_t packed[4];
+  bool big = false;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = c0 + 2 * q;
+    const float a = c < m.K1 ? __ldg(xc + c) : 0.0f;
+    const float b = c + 1 < m.K1 ? __ldg(xc + c + 1) : 0.0f;
+    big |= !(fabsf(a) <= m.feat_bound) || !(fabsf(b) <= m.feat_bound);
+    const __half2 h = __floats2half2_rn(__fmul_rn(a, m.act_scale), __fmul_rn(b, m.act_scale));
+    packed[q] = *reinterpret_cast<const uint32_t*>(&h);
+  }
+  if (big) atomicOr(overflow, 1);
+  uint8_t* tile = X + bin_x_offset(top, cap_tiles) + (j >> 7) * static_cast<int64_t>(top + 1) * kBinTileBytes;
+  *reinterpret_cast<uint4*>(tile + canon_offset(static_cast<int>(j & 127), c0, kTileM)) =
+      make_uint4(packed[0], packed[1], packed[2], packed[3]);
+  if (c0 == 0) {
+    float4* dst = reinterpret_cast<float4*>(meta + static_cast<int64_t>(top) * cap_tiles * kTileM + j);
+    const lsnif_interval v = iv[j];
+    dst[0] = make_float4(__int_as_float(static_cast<int32_t>(j)), v.enter, v.exit, 0.0f);
+    dst[1] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  }
+}
+
 __global__ void __launch_bounds__(128) infer_f32_kernel(const DevModel m, const float* __restrict__ x,
                                                         int64_t n, const lsnif_interval* __restrict__ iv,
-                                                        lsnif_hit* __restrict__ out) {
+                                                        lsnif_hit* __restrict__ out, const int* only_if) {
+  if (only_if && *only_if == 0) return;  // the tcgen05 path answered this call
   const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (j >= n) return;
   const int in = m.K1, hid = m.hidden, no = m.n_out;
@@ -1341,9 +1384,19 @@ cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStrea
 }
 
 cudaError_t launch_infer_f32(const DevModel& m, const float* x, int64_t n, const lsnif_interval* iv,
-                             lsnif_hit* out, cudaStream_t st) {
+                             lsnif_hit* out, cudaStream_t st, const int* only_if) {
   if (n <= 0) return cudaSuccess;
-  infer_f32_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(m, x, n, iv, out);
+  infer_f32_kernel<<<static_cast<unsigned>((n + 127) / 128), 128, 0, st>>>(m, x, n, iv, out, only_if);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_infer_pack(const DevModel& m, const float* x, int64_t n, const lsnif_interval* iv, uint8_t* X,
+                              RowMeta* meta, int32_t* row_counter, int64_t cap_tiles, int* overflow,
+                              cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t total = n * (m.K1P / 8);
+  infer_pack_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(m, x, n, iv, X, meta, row_counter,
+                                                                               cap_tiles, overflow);
   return cudaGetLastError();
 }
 

@@ -88,6 +88,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     lib.lsnif_query_closest.argtypes = [P, P, P, C.c_int64, P, P]
     lib.lsnif_query_any.argtypes = [P, P, P, C.c_int64, P, P]
     lib.lsnif_infer_batch.argtypes = [P, P, C.c_int64, C.c_int64, P, C.c_int64, P, P]
+    lib.lsnif_infer_batch_f32.argtypes = [P, P, C.c_int64, C.c_int64, P, C.c_int64, P, P]
     lib.lsnif_debug_traverse.argtypes = [P, P, C.c_int64] + [P] * 7 + [P]
     lib.lsnif_last_query_stats.argtypes = [P, P, C.POINTER(QueryStats)]
     lib.lsnif_profile_enable.argtypes = [P, C.c_int]
@@ -107,7 +108,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     for name in ("lsnif_model_load", "lsnif_model_destroy", "lsnif_model_get_info", "lsnif_query",
                  "lsnif_query_host", "lsnif_query_wire", "lsnif_query_host_wire",
                  "lsnif_hits_from_wire", "lsnif_query_pairs", "lsnif_query_closest", "lsnif_query_any",
-                 "lsnif_infer_batch", "lsnif_debug_traverse",
+                 "lsnif_infer_batch", "lsnif_infer_batch_f32", "lsnif_debug_traverse",
                  "lsnif_last_query_stats", "lsnif_profile_enable", "lsnif_profile_read",
                  "lsnif_scene_create", "lsnif_scene_destroy", "lsnif_scene_query",
                  "lsnif_scene_query_host", "lsnif_render",
@@ -262,18 +263,20 @@ class GpuModel:
             _stream_ptr(None)))
         return out
 
-    def infer_batch(self, inputs, intervals, stream=None):
+    def infer_batch(self, inputs, intervals, stream=None, exact: bool = False):
         """infer_batch (renderer.cpp:183-226). inputs: CUDA (n, input_width)
-        fp32 — row j is column j of the reference's MatX; intervals (n, 2)."""
+        fp32 — row j is column j of the reference's MatX; intervals (n, 2).
+        The tcgen05 MLP (lsnif_infer_batch), or with exact=True the fp32
+        kernel in the reference's summation order (lsnif_infer_batch_f32)."""
         torch = _torch()
         inputs = inputs.contiguous()
         intervals = intervals.contiguous()
         n = inputs.shape[0]
         rows = inputs.shape[1] if inputs.dim() == 2 else 0
         out = torch.empty((n, 8), dtype=torch.int32, device=inputs.device)
-        _check(load_library().lsnif_infer_batch(self.h, inputs.data_ptr(), rows, n,
-                                                intervals.data_ptr(), intervals.shape[0],
-                                                out.data_ptr(), _stream_ptr(stream)))
+        fn = load_library().lsnif_infer_batch_f32 if exact else load_library().lsnif_infer_batch
+        _check(fn(self.h, inputs.data_ptr(), rows, n, intervals.data_ptr(), intervals.shape[0],
+                  out.data_ptr(), _stream_ptr(stream)))
         return out
 
     # ---- host API (numpy, the reference's by-value vectors) ----

@@ -47,19 +47,58 @@ def test_traverse_bit_exact(gmodel, oracle_teapot, name):
     assert (ref["info"] & 255).sum() > 0
 
 
-def test_infer_batch_fp32(gmodel, oracle_teapot):
-    rays = W.incoherent_rays(8192, gmodel.aabb, seed=11)
+def _infer_inputs(oracle_teapot, box, n=8192, seed=11):
+    rays = W.incoherent_rays(n, box, seed=seed)
     tr = oracle_teapot.trace(rays)
     keep = (tr["info"] >> 9) & 1 == 1
-    x, iv = tr["feat"][keep], tr["interval"][keep]
+    return tr["feat"][keep], tr["interval"][keep]
+
+
+def test_infer_batch_fp32(gmodel, oracle_teapot):
+    """lsnif_infer_batch_f32: fp32 in the reference's summation order, 1e-5."""
+    x, iv = _infer_inputs(oracle_teapot, gmodel.aabb)
     ref = oracle_teapot.infer_batch(x, iv)
     got = lsnif.hits_to_numpy(gmodel.infer_batch(torch.from_numpy(x).cuda(),
-                                                  torch.from_numpy(iv).cuda()))
+                                                  torch.from_numpy(iv).cuda(), exact=True))
     assert np.array_equal(got["flags_material"], ref["flags_material"])
     for k in ("t_world", "normal", "albedo"):
         np.testing.assert_allclose(got[k], ref[k], rtol=1e-5, atol=1e-6)
     with pytest.raises(ValueError):
+        gmodel.infer_batch(torch.from_numpy(x).cuda(), torch.from_numpy(iv[:-1]).cuda(), exact=True)
+
+
+def test_infer_batch_tcgen05(gmodel, oracle_teapot):
+    """lsnif_infer_batch on the tcgen05 MLP: SURVEY App. B tolerances against
+    the oracle (visibility / material >= 99.9%; for rays both call occluded
+    |dt| <= 2e-3 (exit - enter), normal <= 1 degree, albedo <= 2e-3); no
+    PAIR / ACCEPTED flags, as the fp32 form."""
+    x, iv = _infer_inputs(oracle_teapot, gmodel.aabb, n=1 << 16, seed=12)
+    ref = oracle_teapot.infer_batch(x, iv)
+    got = lsnif.hits_to_numpy(gmodel.infer_batch(torch.from_numpy(x).cuda(), torch.from_numpy(iv).cuda()))
+    fg, fr = got["flags_material"], ref["flags_material"]
+    assert not np.any(fg & 5)
+    assert np.mean((fg & 2) == (fr & 2)) >= 0.999
+    assert np.mean((fg >> 8) == (fr >> 8)) >= 0.999
+    both = ((fg & 2) != 0) & ((fr & 2) != 0)
+    span = np.maximum(iv[:, 1] - iv[:, 0], 1e-30)
+    assert np.all(np.abs(got["t_world"] - ref["t_world"])[both] <= 2e-3 * span[both] + 1e-6)
+    nz = both & (np.linalg.norm(ref["normal"], axis=1) > 0)
+    cosang = np.sum(got["normal"][nz] * ref["normal"][nz], axis=1)
+    assert np.all(cosang >= np.cos(np.radians(1.0)))
+    assert np.all(np.abs(got["albedo"] - ref["albedo"])[both] <= 2e-3)
+    with pytest.raises(ValueError):
         gmodel.infer_batch(torch.from_numpy(x).cuda(), torch.from_numpy(iv[:-1]).cuda())
+
+
+def test_infer_batch_out_of_range_inputs_use_fp32(gmodel, oracle_teapot):
+    """Columns beyond the encoder range (not table interpolations) are answered
+    by the fp32 kernel, decided on the device: bit-equal to the exact form."""
+    x, iv = _infer_inputs(oracle_teapot, gmodel.aabb, n=4096, seed=13)
+    x = x * np.float32(1e6)
+    xs, ivs = torch.from_numpy(x).cuda(), torch.from_numpy(iv).cuda()
+    got = lsnif.hits_to_numpy(gmodel.infer_batch(xs, ivs))
+    ref = lsnif.hits_to_numpy(gmodel.infer_batch(xs, ivs, exact=True))
+    assert np.array_equal(got.view(np.uint32), ref.view(np.uint32))
 
 
 def compare_query(got, ref, label):
