@@ -337,21 +337,27 @@ void build_model(lsnif_model_s& M, const lsnif_model_desc& d) {
     const int Vp = V + 2;
     const size_t nbits = static_cast<size_t>(Vp) * Vp * Vp;
     std::vector<uint32_t> stop((nbits + 31) / 32, 0u);
+    // the same cells as 2-bit codes (0 free, 1 occupied, 2 border) for the
+    // query kernel, whose walk tells an occupied cell from the border
+    std::vector<uint32_t> stop2((nbits + 15) / 16, 0u);
     for (int z = 0; z < Vp; ++z)
       for (int y = 0; y < Vp; ++y)
         for (int x = 0; x < Vp; ++x) {
           const bool inside = x >= 1 && x <= V && y >= 1 && y <= V && z >= 1 && z <= V;
-          bool bit = true;
+          uint32_t code = 2u;
           if (inside) {
             const size_t i = static_cast<size_t>(x - 1) + static_cast<size_t>(V) *
                              (static_cast<size_t>(y - 1) + static_cast<size_t>(V) * (z - 1));
-            bit = (d.occupancy[i >> 3] >> (i & 7)) & 1u;
+            code = (d.occupancy[i >> 3] >> (i & 7)) & 1u;
           }
           const size_t j = static_cast<size_t>(x) + static_cast<size_t>(Vp) * (y + static_cast<size_t>(Vp) * z);
-          if (bit) stop[j >> 5] |= 1u << (j & 31);
+          if (code) stop[j >> 5] |= 1u << (j & 31);
+          stop2[j >> 4] |= code << ((j & 15) * 2);
         }
     m.stop = M.upload<uint32_t>(stop.data(), stop.size() * 4);
     m.stop_words = static_cast<int>(stop.size());
+    m.stop2 = M.upload<uint32_t>(stop2.data(), stop2.size() * 4);
+    m.stop2_words = static_cast<int>(stop2.size());
   }
 
   // hash tables: 4 binary16 per entry (8 B, one load per corner)

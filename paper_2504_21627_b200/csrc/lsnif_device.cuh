@@ -49,6 +49,8 @@ struct DevModel {
   const uint32_t* occ;                 // V^3/32 words
   const uint32_t* stop;                // (V+2)^3 bits: occupied cells + the outside border
   int stop_words;
+  const uint32_t* stop2;               // (V+2)^3 2-bit codes: 0 free, 1 occupied, 2 border
+  int stop2_words;
   int x_stages;                        // MLP X-tile ring depth (set at load from the SMEM budget)
   const uint2* tables[kMaxLevels];     // M entries x 4 binary16 (F <= 4, zero padded)
   int hidden, n_out, n_mat, N3;        // N3: layer-3 MMA width (>= n_out, multiple of 16)
@@ -279,6 +281,73 @@ __device__ __forceinline__ void walk_advance(Walk& w, float& tn, bool& p1, bool&
   int dl = p1 ? w.lin[1] : w.lin[0];
   dl = p2 ? w.lin[2] : dl;
   w.idx += static_cast<uint32_t>(dl);
+}
+
+// walk_advance returning the step's padded-index increment instead of the
+// argmin predicates; the increment also names the stepped axis (the pool
+// code below), so no predicate state is carried around the caller's loop.
+__device__ __forceinline__ int walk_advance_dl(Walk& w, float& tn) {
+  const bool p1 = w.tn[1] < w.tn[0];
+  tn = p1 ? w.tn[1] : w.tn[0];
+  const bool p2 = w.tn[2] < tn;
+  tn = p2 ? w.tn[2] : tn;
+  const bool a0 = !p1 && !p2;
+  const bool a1 = p1 && !p2;
+  if (a0) w.tn[0] = __fadd_rn(w.tn[0], w.td[0]);
+  if (a1) w.tn[1] = __fadd_rn(w.tn[1], w.td[1]);
+  if (p2) w.tn[2] = __fadd_rn(w.tn[2], w.td[2]);
+  int dl = p1 ? w.lin[1] : w.lin[0];
+  dl = p2 ? w.lin[2] : dl;
+  w.idx += static_cast<uint32_t>(dl);
+  return dl;
+}
+
+// Trace-kernel stop-code mask size in 32-bit words: one byte per padded cell
+// in the 1024-thread configuration, else 2 bits (16-byte multiple).
+__host__ __device__ __forceinline__ int trace_mask_words(const DevModel& m, int warps_per_block) {
+  return warps_per_block == 32 ? m.stop2_words * 4 : (m.stop2_words + 3) & ~3;
+}
+
+// Stop code of a padded cell in a 2-bit code mask (16 cells per word):
+// 0 free, 1 occupied (emit), 2 border (the walk left the grid, dda.cpp:112).
+__device__ __forceinline__ uint32_t stop_code2(const uint32_t* stop2, uint32_t idx) {
+  return (stop2[idx >> 4] >> ((idx & 15u) << 1)) & 3u;
+}
+
+// One-byte pool code of a boundary point in the query kernel. The walk
+// stores the low byte of the step's padded-index increment (+-1, +-(V+2),
+// +-(V+2)^2: distinct low bytes for every power-of-two V <= 64, none in
+// 0x80..0x83); the start point stores 0x80 | entry axis, or 0x83 when the
+// origin is inside the cell (the "volume" first point, first_is_origin).
+// point_axis_code maps either to: bits 0-1 the entry axis (3: volume), bit 2
+// set for the start point, whose entry plane is round(start V) (dda.cpp:86);
+// a later point crossed the plane nearest to V (o + t d) along the stepped
+// axis (dda.cpp:89-95: t is within a few ulps of the exact crossing, far
+// below half a cell). The plane is rebuilt from t in the encode, so the
+// divergent emit path of the walk is a handful of instructions.
+__device__ __forceinline__ uint32_t start_code(int axis0) {
+  return axis0 < 0 ? 0x83u : (0x80u | static_cast<uint32_t>(axis0));
+}
+__device__ __forceinline__ uint32_t point_axis_code(uint32_t code, int V) {
+  if ((code & 0xfcu) == 0x80u) return (code & 3u) == 3u ? 3u : ((code & 3u) | 4u);
+  const uint32_t vp = static_cast<uint32_t>(V + 2) & 0xffu;
+  return (code == 1u || code == 0xffu) ? 0u : ((code == vp || code == ((0u - vp) & 0xffu)) ? 1u : 2u);
+}
+
+// Entry point of a pooled boundary point (dda.cpp:90-95, 113): o + t d with
+// the entry-axis coordinate snapped to plane / V (axis code as above).
+__device__ __forceinline__ void point_from_code(float t, uint32_t code, const float o[3], const float d[3],
+                                                float fres, float inv_fres, float p[3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) p[a] = __fadd_rn(o[a], __fmul_rn(t, d[a]));
+  const uint32_t axis = code & 3u;
+  if (axis == 3u) return;
+  const float s = __fmul_rn(axis == 0u ? p[0] : axis == 1u ? p[1] : p[2], fres);
+  const float plane = (code & 4u) ? roundf(s) : rintf(s);
+  const float snapped = __fmul_rn(plane, inv_fres);  // == plane / fres (fres a power of two)
+  if (axis == 0u) p[0] = snapped;
+  else if (axis == 1u) p[1] = snapped;
+  else p[2] = snapped;
 }
 
 // Cell coordinates (unpadded, may be -1 or V when outside) of a padded index.

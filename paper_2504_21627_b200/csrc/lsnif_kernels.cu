@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
   const int LF = L * F;
   const int H = m.H;
   const int V = VS ? VS : m.V;
-  const int occ_words = m.stop_words;
+  const int code_words = m.stop2_words;
   // the MLP kernel (launched as a programmatic dependent) may start its
   // prologue while this grid runs; it waits for our completion before reading
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -57,13 +57,15 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
   if (P.n_dev && P.offset >= static_cast<int64_t>(*P.n_dev)) return;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // point pool per warp: entry t (fp32) and code (axis | plane << 2) in
-  // separate arrays, H x 32 each (5 or 6 bytes per point)
-  using code_t = typename std::conditional<(VS != 0 && VS < 64), uint8_t, uint16_t>::type;
-  // stop mask in SMEM: one bit per padded cell, or (1024-thread blocks, one
-  // per SM) one byte per cell, which turns the per-step test into a byte load
+  // point pool per warp: entry t (fp32) and a one-byte code (start_code /
+  // the step's index increment, point_axis_code) in separate arrays, H x 32
+  // each (5 bytes per point)
+  using code_t = uint8_t;
+  // stop codes in SMEM (0 free, 1 occupied, 2 border): 2 bits per padded
+  // cell, or (1024-thread blocks, one per SM) one byte per cell, which turns
+  // the per-step test into a byte load
   constexpr bool kByteMask = TW == 32;
-  const int mask_words = kByteMask ? (occ_words * 32 + 15) / 16 * 4 : (occ_words + 3) & ~3;
+  const int mask_words = trace_mask_words(m, TW);
   float4* lane_ray = reinterpret_cast<float4*>(smem + mask_words) + warp * 64;
   float* pool_t = reinterpret_cast<float*>(smem + mask_words + TW * 64 * 4) + warp * (H * 32);
   code_t* pool_c = reinterpret_cast<code_t*>(pool_t - warp * (H * 32) + TW * H * 32) + warp * (H * 32);
@@ -109,16 +111,16 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
   int64_t next_wb = claimed();
   load_ray(next_wb);
   if (kByteMask) {
-    for (int i = threadIdx.x; i < occ_words * 8; i += blockDim.x) {  // 4 cells per 32-bit store
-      const uint32_t w = __ldg(m.stop + (i >> 3)) >> ((i & 7) * 4);
-      smem[i] = (w & 1u) | ((w & 2u) << 7) | ((w & 4u) << 14) | ((w & 8u) << 21);
+    for (int i = threadIdx.x; i < code_words * 4; i += blockDim.x) {  // 4 cells per 32-bit store
+      const uint32_t w = __ldg(m.stop2 + (i >> 2)) >> ((i & 3) * 8);
+      smem[i] = (w & 3u) | ((w & 0xcu) << 6) | ((w & 0x30u) << 12) | ((w & 0xc0u) << 18);
     }
   } else {
-    for (int i = threadIdx.x; i < occ_words; i += blockDim.x) smem[i] = __ldg(m.stop + i);
+    for (int i = threadIdx.x; i < code_words; i += blockDim.x) smem[i] = __ldg(m.stop2 + i);
   }
-  auto stop_at = [&](uint32_t idx) -> bool {
-    if (kByteMask) return reinterpret_cast<const uint8_t*>(smem)[idx] != 0;
-    return stop_bit(smem, idx);
+  auto stop_at = [&](uint32_t idx) -> uint32_t {
+    if (kByteMask) return reinterpret_cast<const uint8_t*>(smem)[idx];
+    return stop_code2(smem, idx);
   };
   __syncthreads();
   while (next_wb < nwb) {
@@ -149,7 +151,7 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
     if (pair && walk_setup<VS>(m, o, d, t_min, w)) {
       if (stop_at(w.idx)) {  // start cell (always inside the grid)
         fio = w.axis0 < 0;
-        pool_put(lane, pack_point(w.t0, w.axis0, w.plane0));
+        pool_put(lane, make_uint2(__float_as_uint(w.t0), start_code(w.axis0)));
         if (DEBUG) {
           int c[3];
           walk_cell<VS>(m, w.idx, c);
@@ -158,26 +160,19 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
         count = 1;
       }
       float tn;
-      bool p1, p2;
       if (count < H && w.t1 != -__int_as_float(0x7f800000)) {
         // one latch (the advance at the bottom) keeps this a single loop:
-        // lanes at a stop cell emit while the others keep walking
-        walk_advance(w, tn, p1, p2);
+        // lanes at a stop cell emit while the others keep walking; the emit
+        // stores t and the low byte of the step's index increment (the
+        // stepped axis), the entry plane is rebuilt from t in the encode
+        int dl = walk_advance_dl(w, tn);
         for (;;) {
-          if (stop_at(w.idx)) {
-            if (tn > w.t1) break;  // the walk ended before this cell (dda.cpp:106)
-            // The crossed plane of the stepped axis (dda.cpp:89-95: c_new for
-            // +steps, c_new + 1 for -steps) is the integer nearest to
-            // V * (o + tn d) along that axis: tn is within a few ulps of the
-            // exact crossing, far below half a cell. Crossing plane V going
-            // up / plane 0 going down means the set bit is the border: the
-            // walk left the grid (dda.cpp:112).
-            const int axis = p2 ? 2 : (p1 ? 1 : 0);
-            const float oa = p2 ? w.o[2] : (p1 ? w.o[1] : w.o[0]);
-            const float da = p2 ? w.d[2] : (p1 ? w.d[1] : w.d[0]);
-            const int plane = static_cast<int>(rintf(__fmul_rn(__fadd_rn(oa, __fmul_rn(tn, da)), m.fres)));
-            if (plane == (da > 0.0f ? V : 0)) break;
-            pool_put(count * 32 + lane, pack_point(tn, axis, static_cast<float>(plane)));
+          const uint32_t sc = stop_at(w.idx);
+          if (sc != 0u) {
+            // the border (the walk left the grid, dda.cpp:112), or the walk
+            // ended before this cell (dda.cpp:106)
+            if (sc > 1u || tn > w.t1) break;
+            pool_put(count * 32 + lane, make_uint2(__float_as_uint(tn), static_cast<uint32_t>(dl) & 0xffu));
             if (DEBUG) {
               int c[3];
               walk_cell<VS>(m, w.idx, c);
@@ -185,7 +180,7 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
             }
             if (++count >= H) break;  // first-H truncation (dda.cpp:99)
           }
-          walk_advance(w, tn, p1, p2);
+          dl = walk_advance_dl(w, tn);
         }
       }
     }
@@ -247,8 +242,7 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
                             int k, const uint2 e) {
       constexpr bool volume = decltype(VOLT)::value;
       float p[3];
-      bool vol_code;
-      unpack_point(e, ro, rd, m.inv_fres, p, vol_code);
+      point_from_code(__uint_as_float(e.x), point_axis_code(e.y, V), ro, rd, m.fres, m.inv_fres, p);
       float fv[16];
       const int pa = volume ? -1 : plane_axis_of(p, m.fres);
       if (LS == 2 && !volume) {
@@ -1255,11 +1249,8 @@ cudaError_t compute_zero_hit(const DevModel& m, lsnif_hit* host_out) {
 }
 
 size_t trace_smem_bytes(const DevModel& m, int warps) {
-  const size_t occ_words = static_cast<size_t>(m.stop_words);
-  const bool fast = m.L == 2 && m.F == 3 && m.M_pow2 && m.V == 32;  // 1-byte point codes
-  const size_t mask_bytes = warps == 32 ? (occ_words * 32 + 15) / 16 * 16 : ((occ_words + 3) & ~size_t(3)) * 4;
-  return mask_bytes + static_cast<size_t>(warps) * 64 * 16 +
-         static_cast<size_t>(warps) * static_cast<size_t>(m.H) * 32 * (fast ? 5 : 6);
+  return static_cast<size_t>(trace_mask_words(m, warps)) * 4 + static_cast<size_t>(warps) * 64 * 16 +
+         static_cast<size_t>(warps) * static_cast<size_t>(m.H) * 32 * 5;
 }
 
 size_t mlp_smem_bytes(const DevModel& m, int stages) {
