@@ -149,6 +149,9 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
     int count = 0;
     bool fio = false;
     if (pair && walk_setup<VS>(m, o, d, t_min, w)) {
+      // the encode reads the local ray back from SMEM: o, d are dead in the walk
+      lane_ray[2 * lane] = make_float4(w.o[0], w.o[1], w.o[2], 0.0f);
+      lane_ray[2 * lane + 1] = make_float4(w.d[0], w.d[1], w.d[2], 0.0f);
       if (stop_at(w.idx)) {  // start cell (always inside the grid)
         fio = w.axis0 < 0;
         pool_put(lane, make_uint2(__float_as_uint(w.t0), start_code(w.axis0)));
@@ -226,9 +229,9 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
       st_vol += (valid && fio) ? 1u : 0u;
     }
 
-    if (valid) {
-      lane_ray[2 * lane] = make_float4(w.o[0], w.o[1], w.o[2], __int_as_float(row));
-      lane_ray[2 * lane + 1] = make_float4(w.d[0], w.d[1], w.d[2], __int_as_float(bin));
+    if (valid) {  // the row / bin of the stashed local ray
+      reinterpret_cast<int*>(lane_ray)[8 * lane + 3] = row;
+      reinterpret_cast<int*>(lane_ray)[8 * lane + 7] = bin;
     }
     __syncwarp();
     // ---- warp-cooperative encode of the pooled points (encoding.hpp:166-176):
@@ -349,7 +352,11 @@ __global__ void __launch_bounds__(32 * TW, 32 / TW) trace_encode_kernel(const Tr
       encode_point(std::false_type{}, ro, rd, wbatch * 32 + owner, __float_as_int(rq.w), __float_as_int(rr.w), k,
                    pool_get(k * 32 + owner));
     }
-    if (vc) encode_point(std::true_type{}, w.o, w.d, ray_idx, row, bin, 0, pool_get(lane));
+    if (vc) {
+      const float4 sq = lane_ray[2 * lane], sr = lane_ray[2 * lane + 1];
+      const float so[3] = {sq.x, sq.y, sq.z}, sd[3] = {sr.x, sr.y, sr.z};
+      encode_point(std::true_type{}, so, sd, ray_idx, row, bin, 0, pool_get(lane));
+    }
 
     // ---- zero padding of the row tail up to the bin width (encoding.hpp:170)
     if (!DEBUG && valid) {
