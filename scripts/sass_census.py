@@ -43,7 +43,7 @@ tot = collections.Counter()
 for k, c in counts.items():
     tot.update(c)
     name = demangled.get(k, k)
-    name = re.sub(r"\(.*", "", name)[:110]
+    name = re.sub(r"\(.*", "", name.replace("(anonymous namespace)", "anon"))[:110]
     fields = " ".join(f"{key}={c[key]}" for key in KEYS if c[key])
     print(f"{name}: total={c['_total']} {fields}")
 print("ALL: " + " ".join(f"{key}={tot[key]}" for key in ["_total"] + KEYS if tot[key]))
