@@ -146,7 +146,21 @@ struct HostStagingT {
 };
 using HostStaging = HostStagingT<lsnif_hit>;
 
-constexpr int64_t kChunk = int64_t(1) << 21;      // rays per trace/MLP launch pair
+// Rays per trace/MLP launch pair (A/B override LSNIF_CHUNK_LOG2, read once).
+// Fewer, longer launches amortise each launch's fixed costs (stop-mask fill,
+// weight copy and TMEM allocation, both kernels' tails): C5 device rays/s at
+// 2^21 / 2^22 / 2^23 / 2^24 / 2^25 = 5.65 / 5.97 / 6.15 / 6.24 / 6.29 e9. A
+// query's workspace grows with the chunk (per-bin X regions sized for every
+// row: ~9.4 GB of HBM per stream at 2^23, for queries that large).
+inline int64_t chunk_rays() {
+  static const int64_t c = [] {
+    const char* e = std::getenv("LSNIF_CHUNK_LOG2");
+    const int l = e ? std::atoi(e) : 23;
+    return int64_t(1) << (l < 16 ? 16 : (l > 25 ? 25 : l));
+  }();
+  return c;
+}
+#define kChunk chunk_rays()
 constexpr int64_t kHostChunk = int64_t(1) << 17;  // rays per host staging step (LSNIF_HOST_CHUNK overrides)
 
 int64_t host_chunk(int64_t dflt = kHostChunk) {
