@@ -157,13 +157,12 @@ __device__ __forceinline__ bool slab_interval(const float o[3], const float d[3]
 }
 
 // State of one Amanatides-Woo walk (dda.cpp:40-117) in local unit-cube space.
-// The current cell is a linear index into the padded (V+2)^3 "stop" bitmask
-// (x fastest, voxel.hpp:30-34 order shifted by one), whose set bits are the
-// occupied cells plus the one-cell border outside the grid: a single SMEM
-// bit test per step finds both an occupied cell to emit and the walk leaving
-// the grid (dda.cpp:112), which is told apart only on that rare path. The
-// entry plane of a stepped-into cell is derived from the new cell when a point
-// is emitted (dda.cpp:108: c_old+1 == c_new for +steps, c_old for -steps).
+// The current cell is a linear index into the padded (V+2)^3 stop mask (x
+// fastest, voxel.hpp:30-34 order shifted by one), whose non-zero codes are
+// the occupied cells (1) and the one-cell border outside the grid (2): one
+// SMEM load per step finds both an occupied cell to emit and the walk leaving
+// the grid (dda.cpp:112). The query kernel keeps 2-bit / byte codes
+// (stop2); the trainer's encode the plain bitmask (stop) with walk_step.
 struct Walk {
   float o[3], d[3];    // nudged local origin and local direction
   float t1;
@@ -268,24 +267,9 @@ __device__ __forceinline__ bool walk_step(Walk& w, float& tn, bool& p1, bool& p2
 // that cell's entry t exceeds t1, and no cell in between emits; the caller
 // tests tn > t1 once per stop cell. Any moving walk reaches the border within
 // 3 (V + 2) advances; not for a walk with no moving axis (t1 = -inf).
-__device__ __forceinline__ void walk_advance(Walk& w, float& tn, bool& p1, bool& p2) {
-  p1 = w.tn[1] < w.tn[0];
-  tn = p1 ? w.tn[1] : w.tn[0];
-  p2 = w.tn[2] < tn;
-  tn = p2 ? w.tn[2] : tn;
-  const bool a0 = !p1 && !p2;
-  const bool a1 = p1 && !p2;
-  if (a0) w.tn[0] = __fadd_rn(w.tn[0], w.td[0]);
-  if (a1) w.tn[1] = __fadd_rn(w.tn[1], w.td[1]);
-  if (p2) w.tn[2] = __fadd_rn(w.tn[2], w.td[2]);
-  int dl = p1 ? w.lin[1] : w.lin[0];
-  dl = p2 ? w.lin[2] : dl;
-  w.idx += static_cast<uint32_t>(dl);
-}
-
-// walk_advance returning the step's padded-index increment instead of the
-// argmin predicates; the increment also names the stepped axis (the pool
-// code below), so no predicate state is carried around the caller's loop.
+// Returns the step's padded-index increment, which also names the stepped
+// axis (the pool code below), so no predicate state is carried around the
+// caller's loop.
 __device__ __forceinline__ int walk_advance_dl(Walk& w, float& tn) {
   const bool p1 = w.tn[1] < w.tn[0];
   tn = p1 ? w.tn[1] : w.tn[0];
