@@ -27,7 +27,9 @@ gm.query_pairs(rays, ivs, lsnif.CLOSEST)
 gm.query_host(rays.cpu().numpy().view(lsnif.RAY_DTYPE).reshape(-1), lsnif.ANY)
 x = torch.zeros((64, gm.input_width), dtype=torch.float32, device="cuda")
 iv = torch.zeros((64, 2), dtype=torch.float32, device="cuda")
-gm.infer_batch(x, iv)
+gm.infer_batch(x, iv)                          # tcgen05 MLP (infer_pack_kernel + mlp_tc_kernel)
+gm.infer_batch(x, iv, exact=True)              # fp32 kernel
+gm.infer_batch(torch.full_like(x, 1e6), iv)    # out-of-range inputs: the device-side fp32 fallback
 models = [lsnif.GpuModel(os.path.join(gold, n + ".lsnif")) for n in W.RENDER_MODELS]
 w2o = W.render_world_to_object()
 scene = lsnif.GpuScene([(models[i], w2o[i]) for i in range(len(models))])
