@@ -161,7 +161,11 @@ inline int64_t chunk_rays() {
   return c;
 }
 #define kChunk chunk_rays()
-constexpr int64_t kHostChunk = int64_t(1) << 17;  // rays per host staging step (LSNIF_HOST_CHUNK overrides)
+// Largest host staging step in rays (LSNIF_HOST_CHUNK overrides); a call is
+// cut into ~8 steps of at least 64K rays up to this cap. Larger steps cut the
+// per-copy overhead of big calls: C5 e2e 1.44e9 -> 1.63e9 rays/s, C3 1.44 ->
+// 1.51e9, C2 1.18 -> 1.29e9 with a 2^21 cap instead of 2^17 (2^22: no better).
+constexpr int64_t kHostChunk = int64_t(1) << 21;
 
 int64_t host_chunk(int64_t dflt = kHostChunk) {
   const char* e = std::getenv("LSNIF_HOST_CHUNK");
@@ -924,7 +928,7 @@ lsnif_status lsnif_scene_query_host(lsnif_scene scene, const lsnif_ray* h_rays, 
     std::lock_guard<std::mutex> lock(scene->staging_mu);
     // larger steps than the single-model path: a scene chunk is ~4 launches
     // per instance (scripts/scene_e2e_probe.py: C4 2^17 3.77 ms, 2^18 3.13 ms)
-    host_round_trip(scene->staging, 2 * kHostChunk, h_rays, n, h_hits, static_cast<cudaStream_t>(stream),
+    host_round_trip(scene->staging, int64_t(1) << 18, h_rays, n, h_hits, static_cast<cudaStream_t>(stream),
                     [&](const lsnif_ray* r, int64_t cn, lsnif_scene_hit* h, cudaStream_t st) {
                       lsnif_api::scene_query_async(scene, r, cn, nullptr, mode, h, st);
                     });
