@@ -326,16 +326,12 @@ class CpuArm:
             return self.m.scene_query(rays, mode, 0)
         return self.m.narrow_phase(rays, mode, 0)
 
-    def best_time(self, rays, mode: int, reps: int) -> float:
-        if self.kind == "reference":
-            return self.m.time_scene_query(rays, mode, 0, reps)
-        return self.m.time_narrow_phase(rays, mode, 0, reps)
-
 
 def time_cpu_sets(arm: "CpuArm", sets, target_s: float):
     """Times the CPU path (all host threads) over the ray sets [(rays, mode),
-    ...] answered back to back: one untimed pass, then repeated passes (best
-    of) spanning ~target_s of CPU work. Returns (rays/s, info)."""
+    ...] answered back to back: one untimed pass, then repeated passes
+    spanning ~target_s of CPU work; the rate is over their total time (the
+    mean pass, as the --impl reference arm reports). Returns (rays/s, info)."""
     n = sum(len(r) for r, _ in sets)
     t0 = time.perf_counter()
     for r, mode in sets:
@@ -343,7 +339,12 @@ def time_cpu_sets(arm: "CpuArm", sets, target_s: float):
             arm.run(r, mode)
     one = max(time.perf_counter() - t0, 1e-6)
     reps = max(1, min(200, int(round(target_s / one))))
-    total = sum(arm.best_time(r, mode, reps) for r, mode in sets if len(r))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        for r, mode in sets:
+            if len(r):
+                arm.run(r, mode)
+    total = (time.perf_counter() - t0) / reps
     return n / total, {"rays": n, "seconds": reps * total, "reps": reps}
 
 
@@ -977,7 +978,7 @@ def run_c5(args, ctx) -> None:
                 line["cpu_baseline"] = {
                     "value": rate, "unit": UNIT, "cores": arm.cores, "kind": arm.kind,
                     "sample": f"every {C5_CPU_STRIDE}th ray of the C5 frame ({info['rays']} rays, the "
-                              f"reference arm's rays), best of {info['reps']} passes (~{info['seconds']:.1f} s "
+                              f"reference arm's rays), mean of {info['reps']} passes (~{info['seconds']:.1f} s "
                               f"of CPU work)", "what": arm.what}
                 line["cpu_baseline"].update(cpu_detail(rate, arm.cores, pairs_fraction(arm.m, srays),
                                                        model.info.hidden, model.input_width, 8 + model.info.n_mat))
@@ -1097,7 +1098,7 @@ def run_single(args, ctx) -> None:
                     smp = f"the whole frame: {len(primary)} primary + {len(shadow)} shadow rays"
                 rate, info = time_cpu_sets(arm, sets, args.cpu_seconds)
                 line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": arm.cores, "kind": arm.kind,
-                                        "sample": f"{smp}, best of {info['reps']} passes "
+                                        "sample": f"{smp}, mean of {info['reps']} passes "
                                                   f"(~{info['seconds']:.1f} s of CPU work)", "what": arm.what}
                 line["cpu_baseline"].update(cpu_detail(rate, arm.cores,
                                                        pairs_fraction(arm.m, np.concatenate([r for r, _ in sets])),
