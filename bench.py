@@ -686,6 +686,12 @@ class Ctx:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
         self.gloo = args.dist_backend == "gloo"
+        if self.world > 1 and not self.gloo:
+            # leave SMs to NCCL: the persistent query kernels fill every SM they
+            # are given, so the result gather's kernels (side stream) would wait
+            # for each piece's query to finish instead of overlapping the next
+            # one (lsnif_dev::reserved_sms; read once by the library)
+            os.environ.setdefault("LSNIF_RESERVE_SMS", "8")
         self.gpu = 0 if self.gloo else self.local_rank
         torch.cuda.set_device(self.gpu)
         self.dev = torch.device("cuda", self.gpu)
@@ -945,6 +951,7 @@ def run_c5(args, ctx) -> None:
             "config": {"workload": WORKLOADS["c5"] if total == C5_RAYS else
                        WORKLOADS["c5"] + f" [TEST SIZE: {total} rays]",
                        "rays_per_step": total, "rays_per_gpu": sizes, "pieces_per_band": pieces,
+                       "query_sms_left_to_the_gather": int(os.environ.get("LSNIF_RESERVE_SMS", "0")),
                        "result_record_bytes": 16,
                        "l2": "inputs (4.25 GB of rays) far larger than L2; also flushed between timed steps "
                              "(256 MiB write outside the events)",

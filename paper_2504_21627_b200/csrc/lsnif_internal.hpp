@@ -109,6 +109,13 @@ cudaError_t launch_merge(const DevModel& m, const InstanceParams& ip, const lsni
 size_t mlp_smem_bytes(const DevModel& m, int x_stages);
 // Deepest X ring (4..2 stages) whose SMEM fits smem_limit; 0 if none does.
 int mlp_x_stages(const DevModel& m, size_t smem_limit);
+// SMs the persistent query kernels leave free (LSNIF_RESERVE_SMS, read once;
+// default 0). Both query kernels fill every SM they are given (the trace
+// kernel's 1024-thread block takes the whole register file, the MLP CTA most
+// of the shared memory), so a collective's kernels launched concurrently on
+// another stream (the multi-GPU result gather) would otherwise wait for the
+// query to finish instead of overlapping it.
+int reserved_sms();
 cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st);
 cudaError_t launch_mlp(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st);
 cudaError_t launch_infer_pack(const DevModel& m, const float* x, int64_t n, const lsnif_interval* iv, uint8_t* X,

@@ -1322,11 +1322,20 @@ static cudaError_t launch_trace_t(const TraceParams& p, cudaStream_t st) {
     cfg.dev = dev;
     cfg.smem = smem;
   }
-  const int sms = cfg.sms, per_sm = cfg.per_sm;
+  const int sms = std::max(1, cfg.sms - reserved_sms()), per_sm = cfg.per_sm;
   const int64_t blocks = (p.n + 32 * TW - 1) / (32 * TW);  // one 32-ray batch per warp
   const unsigned grid = static_cast<unsigned>(std::min<int64_t>(blocks, static_cast<int64_t>(sms) * std::max(per_sm, 1)));
   kern<<<grid, 32 * TW, smem, st>>>(p);
   return cudaGetLastError();
+}
+
+int reserved_sms() {
+  static const int r = [] {
+    const char* e = std::getenv("LSNIF_RESERVE_SMS");
+    const int v = e ? std::atoi(e) : 0;
+    return v < 0 ? 0 : (v > 64 ? 64 : v);
+  }();
+  return r;
 }
 
 cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st) {
@@ -1347,7 +1356,7 @@ cudaError_t launch_trace(const TraceParams& p, bool debug, cudaStream_t st) {
 template <int HID, int NS>
 static cudaError_t launch_mlp_t(const MlpParams& p, int max_tiles, int num_sms, cudaStream_t st) {
   const size_t smem = mlp_smem_bytes(p.m, p.m.x_stages);
-  const unsigned grid = static_cast<unsigned>(std::min(max_tiles, num_sms));
+  const unsigned grid = static_cast<unsigned>(std::min(max_tiles, std::max(1, num_sms - reserved_sms())));
   thread_local LaunchCfg c;
   int dev = 0;
   cudaError_t de = cudaGetDevice(&dev);
