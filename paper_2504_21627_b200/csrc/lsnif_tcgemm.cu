@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 #include <vector>
 
 #include "lsnif_internal.hpp"
@@ -78,7 +79,9 @@ struct GemmArgs {
   int partial;      // write split partials instead of C
 };
 
-template <int BN>
+// VA / VB: the operand is k-contiguous with 16-byte aligned rows (stride 1
+// along k, row stride a multiple of 4 floats): 16-byte loads.
+template <int BN, bool VA, bool VB>
 __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1) tcgemm_kernel(const GemmArgs g) {
   constexpr uint32_t kStageBytes = stage_bytes<BN>();
   constexpr uint32_t kBOpBytes = BN * kBK * 4;
@@ -126,16 +129,28 @@ __global__ void __launch_bounds__(kThreads, BN == 64 ? 2 : 1) tcgemm_kernel(cons
     const int rb = tid % BN, kb0 = (tid / BN) * kBk;
     const int n = n0 + rb;
     float a[kBK], b[kBk];  // all of the stage's loads in flight before any split / store
+    // 4 consecutive k of one row: a 16-byte load when the operand allows it
+    // and the group lies inside the K range, else element by element
+    auto load4 = [&](auto VEC, const float* base_row, int64_t sk, bool row_ok, int k, float* dst) {
+      if (decltype(VEC)::value && row_ok && k + 3 < k_end) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(base_row + k));
+        dst[0] = v.x;
+        dst[1] = v.y;
+        dst[2] = v.z;
+        dst[3] = v.w;
+      } else {
 #pragma unroll
-    for (int kk = 0; kk < kBK; ++kk) {
-      const int k = k0 + kk;
-      a[kk] = (m < g.M && k < k_end) ? __ldg(g.A + m * g.sam + k * g.sak) : 0.0f;
-    }
+        for (int q = 0; q < 4; ++q) dst[q] = (row_ok && k + q < k_end) ? __ldg(base_row + (k + q) * sk) : 0.0f;
+      }
+    };
+    const float* arow = g.A + static_cast<int64_t>(m < g.M ? m : 0) * g.sam;
+    const float* brow = g.B + static_cast<int64_t>(n < g.N ? n : 0) * g.sbn;
 #pragma unroll
-    for (int kk = 0; kk < kBk; ++kk) {
-      const int k = k0 + kb0 + kk;
-      b[kk] = (n < g.N && k < k_end) ? __ldg(g.B + n * g.sbn + k * g.sbk) : 0.0f;
-    }
+    for (int kk = 0; kk < kBK; kk += 4)
+      load4(std::integral_constant<bool, VA>{}, arow, g.sak, m < g.M, k0 + kk, a + kk);
+#pragma unroll
+    for (int kk = 0; kk < kBk; kk += 4)
+      load4(std::integral_constant<bool, VB>{}, brow, g.sbk, n < g.N, k0 + kb0 + kk, b + kk);
 #pragma unroll
     for (int kk = 0; kk < kBK; kk += 4) split_store(st, st + kOpBytes, canon32<kBM>(tid, kk), a + kk);
 #pragma unroll
@@ -240,9 +255,6 @@ cudaError_t tcgemm_colmajor(bool ta, bool tb, int mm, int nn, int kk, const floa
   // 128 x 128 output tiles (128 x 64 tiles, two CTAs per SM, measured slower
   // on the training step: 2.80 vs 2.69 ms at batch 65,536)
   constexpr int bn = 128;
-  cudaError_t e = cudaFuncSetAttribute(tcgemm_kernel<bn>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem_bytes<bn>()));  // per device; cheap
-  if (e != cudaSuccess) return e;
   GemmArgs g{};
   // op(A)(m, k): column-major A is A[i + j lda]; op(A) = A -> (m, k) = A[m + k lda]
   g.A = A;
@@ -273,8 +285,19 @@ cudaError_t tcgemm_colmajor(bool ta, bool tb, int mm, int nn, int kk, const floa
   g.partial = splits > 1;
   if (splits > 1) g.C = work;
   dim3 grid((mm + kBM - 1) / kBM, (nn + bn - 1) / bn, splits);
-  tcgemm_kernel<bn><<<grid, kThreads, smem_bytes<bn>(), st>>>(g);
-  e = cudaGetLastError();
+  auto aligned = [](const float* p, int64_t row_stride, int64_t k_stride) {
+    return k_stride == 1 && row_stride % 4 == 0 && (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+  };
+  const bool va = aligned(A, g.sam, g.sak), vb = aligned(B, g.sbn, g.sbk);
+  auto launch = [&](auto kern) {
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           static_cast<int>(smem_bytes<bn>()));  // per device; cheap
+    if (err != cudaSuccess) return err;
+    kern<<<grid, kThreads, smem_bytes<bn>(), st>>>(g);
+    return cudaGetLastError();
+  };
+  cudaError_t e = va ? (vb ? launch(tcgemm_kernel<bn, true, true>) : launch(tcgemm_kernel<bn, true, false>))
+                     : (vb ? launch(tcgemm_kernel<bn, false, true>) : launch(tcgemm_kernel<bn, false, false>));
   if (e != cudaSuccess || splits == 1) return e;
   const int64_t total = static_cast<int64_t>(mm) * nn;
   split_sum_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, st>>>(work, splits, mm, nn, C, 1, ldc, 0);
