@@ -269,8 +269,10 @@ class GpuModel:
         The tcgen05 MLP (lsnif_infer_batch), or with exact=True the fp32
         kernel in the reference's summation order (lsnif_infer_batch_f32)."""
         torch = _torch()
-        inputs = inputs.contiguous()
-        intervals = intervals.contiguous()
+        for name, t in (("inputs", inputs), ("intervals", intervals)):
+            if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+                raise ValueError(f"{name} must be a contiguous float32 CUDA tensor (no implicit copies: a "
+                                 "temporary could be freed before the asynchronous launch reads it)")
         n = inputs.shape[0]
         rows = inputs.shape[1] if inputs.dim() == 2 else 0
         out = torch.empty((n, 8), dtype=torch.int32, device=inputs.device)
