@@ -1,18 +1,20 @@
 // LSNIF query kernels for sm_100a.
 //
 //  trace_encode_kernel<DEBUG>  one thread per ray: frame-box pair test,
-//      3D-DDA over the SMEM-resident occupancy bitset (points pooled per
-//      warp in SMEM), then a warp-cooperative encode of the pooled points
+//      3D-DDA over the SMEM-resident stop codes (points pooled per warp in
+//      SMEM), then a warp-cooperative encode of the pooled points
 //      (full SIMT efficiency regardless of per-ray point counts). Rays with
 //      >= 1 point get a compacted row of the fp16 MLP operand X, written in
 //      the UMMA canonical tile layout; other rays are answered directly.
 //      DEBUG=true writes the bit-exactness probe instead of X.
 //  mlp_tc_kernel   per 128-row tile: bulk-copy X into SMEM, three
 //      tcgen05.mma layers (fp16 x fp16 -> fp32 in TMEM, biases folded in as
-//      a constant operand column), leaky-ReLU epilogues TMEM -> regs -> SMEM,
-//      head decode + accept rule in the last epilogue, results scattered to
-//      the caller's hit array.
-//  infer_f32_kernel  fp32 CUDA-core infer_batch (renderer.cpp:183-226).
+//      a constant operand column), leaky-ReLU epilogues TMEM -> regs -> TMEM
+//      (half2), head decode + accept rule in the last epilogue, results
+//      scattered to the caller's hit array.
+//  infer_pack_kernel  lsnif_infer_batch's columns -> X tiles for mlp_tc_kernel.
+//  infer_f32_kernel  fp32 CUDA-core infer_batch (renderer.cpp:183-226), the
+//      reference summation order (validation and out-of-range fallback).
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -30,9 +32,9 @@ namespace lsnif_dev {
 
 // ======================================================= trace + encode
 
-// Persistent: each block loads the occupancy bitset once and loops over
-// 128-ray batches. Per warp: DDA per lane (points -> 8-byte pool entries),
-// then a warp-cooperative encode of all pooled points. LS/FS: compile-time
+// Persistent: each block loads the stop codes once; its warps claim 32-ray
+// batches. Per warp: DDA per lane (points -> 5-byte pool entries), then a
+// warp-cooperative encode of all pooled points. LS/FS: compile-time
 // level/feature counts (0 = read from the model); POW2: M is a power of two.
 // TW: warps per block. Every block holds one SMEM copy of the stop mask, so
 // large blocks leave more of the unified L1 to the hash-table gathers and fill
