@@ -314,6 +314,17 @@ def test_generic_configuration_parity(tmp_path, V, H, levels, F, M, hidden, n_ma
     vis, mat, both, dt = compare_query(g, q, f"V{V}")
     assert vis >= 0.999 and mat >= 0.999, (vis, mat)
     assert np.all(dt[both] <= 2e-3 * span[both] + 1e-6)
+    # lsnif_infer_batch (tcgen05 MLP at this hidden width / output count) on
+    # the oracle's encoded columns, against the oracle's infer_batch
+    keep = (ref["info"] >> 9) & 1 == 1
+    x, iv = ref["feat"][keep], ref["interval"][keep]
+    ri = om.infer_batch(x, iv)
+    gi = lsnif.hits_to_numpy(gm.infer_batch(torch.from_numpy(x).cuda(), torch.from_numpy(iv).cuda()))
+    assert np.mean((gi["flags_material"] & 2) == (ri["flags_material"] & 2)) >= 0.999
+    assert np.mean((gi["flags_material"] >> 8) == (ri["flags_material"] >> 8)) >= 0.999
+    bi = ((gi["flags_material"] & 2) != 0) & ((ri["flags_material"] & 2) != 0)
+    si = np.maximum(iv[:, 1] - iv[:, 0], 1e-30)
+    assert np.all(np.abs(gi["t_world"] - ri["t_world"])[bi] <= 2e-3 * si[bi] + 1e-6)
 
 
 def test_fast_path_max_hit_cap_large_launch(tmp_path, oracle_teapot):
