@@ -9,5 +9,5 @@ python - "$TAG" "$VAR" <<'PY'
 import json, sys
 for l in open(f"gpurun_out/{sys.argv[1]}_env.jsonl"):
     r = json.loads(l)
-    print(f"{sys.argv[2]}={r[sys.argv[2]]:4s} {r['set']:9s} trace {r['trace_ms']*1e3:8.1f} us  mlp {r['mlp_ms']*1e3:7.1f} us  query {r['query_ms']*1e3:8.1f} us")
+    print(f"{sys.argv[2]}={r[sys.argv[2]]:4s} {r['set']:9s} trace {r['trace_ms']*1e3:8.1f} us  bin {r.get('bin_ms',0)*1e3:6.1f} us  mlp {r['mlp_ms']*1e3:7.1f} us  query {r['query_ms']*1e3:8.1f} us")
 PY

@@ -48,7 +48,8 @@ for lib in libs:
             p = gm.profile_read(reset=True)
             gm.profile_enable(False)
             r = dict(lib=os.path.basename(lib), drain=int(dr), set=name, rays=d.shape[0],
-                     trace_ms=p["trace_ms"] / reps, mlp_ms=p["mlp_ms"] / reps)
+                     trace_ms=p["trace_ms"] / reps, mlp_ms=p["mlp_ms"] / reps,
+                     bin_ms=p.get("bin_ms", 0.0) / reps, sort=os.environ.get("LSNIF_RAY_SORT", ""))
             r["grays_s_trace"] = d.shape[0] / r["trace_ms"] / 1e6
             r["query_ms"] = tot / reps
             r["carve"] = os.environ.get("LSNIF_TRACE_CARVEOUT", "")
