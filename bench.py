@@ -809,6 +809,38 @@ def kernel_roofline(model, prof, steps: int, n_rays: int, rows: int, pts: int, v
     return roof, kernels, mlp_flops
 
 
+def copy_only_seconds(pin_rays, host_frame, off: int, n: int, chunk: int = 1 << 21, slots: int = 4) -> float:
+    """The e2e path's PCIe ceiling: lsnif_query_host_wire's copy schedule
+    (chunked H2D of 32 B rays, D2H of 16 B results, one stream per slot)
+    without the kernels; best of 2 frames, device-timed."""
+    import torch
+    src = pin_rays.view(torch.uint8).reshape(-1)[: n * 32]
+    dst = host_frame.view(torch.uint8).reshape(-1)[off * 16:(off + n) * 16]
+    d_in = [torch.empty(chunk * 32, dtype=torch.uint8, device="cuda") for _ in range(slots)]
+    d_out = [torch.empty(chunk * 16, dtype=torch.uint8, device="cuda") for _ in range(slots)]
+    streams = [torch.cuda.Stream() for _ in range(slots)]
+    cur = torch.cuda.current_stream()
+    best = float("inf")
+    for _ in range(2):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for s_ in streams:
+            s_.wait_stream(cur)
+        for i, s0 in enumerate(range(0, n, chunk)):
+            c = min(chunk, n - s0)
+            k = i % slots
+            with torch.cuda.stream(streams[k]):
+                d_in[k][: c * 32].copy_(src[s0 * 32:(s0 + c) * 32], non_blocking=True)
+                dst[s0 * 16:(s0 + c) * 16].copy_(d_out[k][: c * 16], non_blocking=True)
+        for s_ in streams:
+            cur.wait_stream(s_)
+        b.record()
+        torch.cuda.synchronize()
+        best = min(best, a.elapsed_time(b) / 1e3)
+    del d_in, d_out
+    return best
+
+
 def run_c5(args, ctx) -> None:
     """C5: one 132.7M-ray frame split into row bands (one per rank); see the
     module docstring."""
@@ -939,6 +971,8 @@ def run_c5(args, ctx) -> None:
         if args.dump:
             np.save(args.dump, d_host.numpy())
     ctx.barrier()
+    # the PCIe ceiling of the same host path (overwrites the host frame)
+    ceil_s = ctx.max_over_ranks(copy_only_seconds(pin_rays, host_frame, off, band))
 
     if rank == 0:
         peaks = load_peaks()
@@ -970,7 +1004,10 @@ def run_c5(args, ctx) -> None:
                                                1e3 * max(per_step)],
                     "api": "lsnif_query_host_wire per rank (pinned host rays -> chunked H2D / query / D2H of "
                            "16 B wire results) into " + host_note,
-                    "bit_identical_to_device_frame": same},
+                    "bit_identical_to_device_frame": same,
+                    "copy_only_ceiling": {"value": total / ceil_s, "unit": UNIT, "frac": e2e_value * ceil_s / total,
+                                          "how": "the same chunked H2D (2^21 rays) / D2H schedule over 4 stream "
+                                                 "slots with no kernels, best of 2, max over ranks"}},
             "gpu_launches": int(launches),
             "clocks": clocks,
         }
