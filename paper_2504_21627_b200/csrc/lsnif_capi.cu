@@ -1314,3 +1314,7 @@ lsnif_status lsnif_last_query_stats(lsnif_model model, void* stream, lsnif_query
 }
 
 }  // extern "C"
+
+#ifdef LSNIF_PROBE  // A/B probes only (scripts/micro/dda_occupancy_probe.cuh)
+const lsnif_dev::DevModel& lsnif_probe_devmodel(lsnif_model m) { return m->dm; }
+#endif

@@ -1410,3 +1410,8 @@ cudaError_t launch_infer_pack(const DevModel& m, const float* x, int64_t n, cons
 }
 
 }  // namespace lsnif_dev
+
+#ifdef LSNIF_PROBE  // A/B probes only, never in the product build
+const lsnif_dev::DevModel& lsnif_probe_devmodel(lsnif_model m);
+#include "../../scripts/micro/dda_occupancy_probe.cuh"
+#endif
