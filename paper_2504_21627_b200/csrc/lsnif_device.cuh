@@ -749,8 +749,9 @@ __device__ __forceinline__ void store_result(void* out, int64_t i, bool wire, co
 // Byte offset of element (row, col) of an fp16 operand tile in the UMMA
 // K-major no-swizzle canonical layout: 8x8 core matrices (128 B), rows
 // grouped by 8 at stride 128 B (SBO), K chunks of 8 at stride rows*16 B (LBO).
+// Within a K chunk the row term (row >> 3) * 128 + (row & 7) * 16 is row * 16.
 __device__ __host__ __forceinline__ uint32_t canon_offset(int row, int col, int rows) {
-  return static_cast<uint32_t>((col >> 3) * rows * 16 + (row >> 3) * 128 + (row & 7) * 16 + (col & 7) * 2);
+  return static_cast<uint32_t>(((col >> 3) * rows + row) * 16 + (col & 7) * 2);
 }
 
 }  // namespace lsnif_dev
