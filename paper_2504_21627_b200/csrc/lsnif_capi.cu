@@ -92,6 +92,7 @@ float half_bits_to_float(uint16_t h) {  // IEEE binary16 -> fp32 (exact)
 struct Workspace {
   uint8_t* X = nullptr;
   size_t x_tiles = 0;
+  int64_t chunk = 0;  // rays per trace/MLP launch pair (pick_chunk)
   RowMeta* meta = nullptr;
   size_t meta_cap = 0;
   uint8_t* counters = nullptr;  // per chunk: u64 batch counter + one i32 row counter per K bin
@@ -146,21 +147,22 @@ struct HostStagingT {
 };
 using HostStaging = HostStagingT<lsnif_hit>;
 
-// Rays per trace/MLP launch pair (A/B override LSNIF_CHUNK_LOG2, read once).
-// Fewer, longer launches amortise each launch's fixed costs (stop-mask fill,
+// Rays per trace/MLP launch pair, chosen per stream workspace (pick_chunk):
+// fewer, longer launches amortise each launch's fixed costs (stop-mask fill,
 // weight copy and TMEM allocation, both kernels' tails): C5 device rays/s at
-// 2^21 / 2^22 / 2^23 / 2^24 / 2^25 = 5.65 / 5.97 / 6.15 / 6.24 / 6.29 e9. A
-// query's workspace grows with the chunk (per-bin X regions sized for every
-// row: ~9.4 GB of HBM per stream at 2^23, for queries that large).
-inline int64_t chunk_rays() {
+// 2^21 / 2^22 / 2^23 / 2^24 / 2^25 = 5.65 / 5.97 / 6.15 / 6.25 / 6.29 e9. The
+// workspace grows with the launch (per-bin X regions sized for every row:
+// ~9.4 GB at 2^23 rows, ~18.8 GB at 2^24, only for queries that large).
+// LSNIF_CHUNK_LOG2 (read once) fixes the size.
+inline int64_t chunk_override() {
   static const int64_t c = [] {
     const char* e = std::getenv("LSNIF_CHUNK_LOG2");
-    const int l = e ? std::atoi(e) : 23;
+    if (!e) return int64_t(0);
+    const int l = std::atoi(e);
     return int64_t(1) << (l < 16 ? 16 : (l > 25 ? 25 : l));
   }();
   return c;
 }
-#define kChunk chunk_rays()
 // Largest host staging step in rays (LSNIF_HOST_CHUNK overrides); a call is
 // cut into ~8 steps of at least 64K rays up to this cap. Larger steps cut the
 // per-copy overhead of big calls: C5 e2e 1.44e9 -> 1.63e9 rays/s, C3 1.44 ->
@@ -224,7 +226,7 @@ void host_round_trip(std::unique_ptr<HostStagingT<Hit>>& staging, int64_t chunk,
   for (int i = 0; i < kSlots; ++i) ck(cudaStreamSynchronize(S.streams[i]), "cudaStreamSynchronize");
 }
 
-constexpr size_t kMaxChunks = 1024;                // chunks per query (2^31 rays / kChunk)
+constexpr size_t kMaxChunks = 1024;                // chunks per query (>= 2^31 rays / 2^21)
 // Counter block, zeroed by one memset per query (only the chunks it uses):
 // 4 x u64 stats, then per chunk {u64 batch counter, i32 row counter per K bin}.
 constexpr size_t kStatsBytes = 32;
@@ -264,6 +266,20 @@ struct lsnif_model_s {
     return static_cast<T*>(p);
   }
 
+  // Workspace bytes for launches of `rows` rays (X regions + row meta).
+  size_t workspace_bytes(int64_t rows) const {
+    const int64_t tiles = (rows + kTileM - 1) / kTileM;
+    return lsnif_dev::bin_x_offset(dm.n_bins, tiles) + static_cast<size_t>(dm.n_bins) * tiles * kTileM * sizeof(RowMeta);
+  }
+  // 2^24-ray launches while their workspace is at most a quarter of the free
+  // HBM (decided once per stream), else 2^23.
+  int64_t pick_chunk() const {
+    if (const int64_t c = chunk_override()) return c;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return int64_t(1) << 23;
+    return workspace_bytes(int64_t(1) << 24) * 4 <= free_b ? int64_t(1) << 24 : int64_t(1) << 23;
+  }
+
   Workspace& workspace(cudaStream_t st, int64_t n) {
     std::lock_guard<std::mutex> lock(mu);
     auto& slot = ws[st];
@@ -272,10 +288,11 @@ struct lsnif_model_s {
       // one allocation, reset by a single memset per query
       ck(cudaMalloc(&slot->stats, kCounterBytes), "cudaMalloc(counters)");
       slot->counters = reinterpret_cast<uint8_t*>(slot->stats) + kStatsBytes;
+      slot->chunk = pick_chunk();
     }
     Workspace& w = *slot;
     // X / meta: one region per K bin, each able to hold every row of a chunk
-    const int64_t rows = std::min<int64_t>(n, kChunk);
+    const int64_t rows = std::min<int64_t>(n, w.chunk);
     const size_t tiles = static_cast<size_t>((rows + kTileM - 1) / kTileM);
     if (tiles > w.x_tiles) {
       cudaFree(w.X);
@@ -670,6 +687,7 @@ void run_query(lsnif_model_s& M, const lsnif_ray* d_rays, int64_t n, int mode, v
   if (n > INT32_MAX) fail(LSNIF_INVALID_ARGUMENT, "more than 2^31-1 rays in one call");
   ck(cudaSetDevice(M.device), "cudaSetDevice");
   Workspace& w = M.workspace(st, std::max<int64_t>(n, 1));
+  const int64_t kChunk = w.chunk;
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   if (static_cast<size_t>(nchunks) > kMaxChunks) fail(LSNIF_INVALID_ARGUMENT, "too many rays in one call");
   ck(cudaMemsetAsync(w.stats, 0, kStatsBytes + kChunkCounterBytes * std::max<int64_t>(nchunks, 1), st),
@@ -1168,6 +1186,7 @@ lsnif_status lsnif_infer_batch(lsnif_model model, const float* d_inputs, int64_t
     lsnif_model_s& M = *model;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     Workspace& w = M.workspace(st, n);
+    const int64_t kChunk = w.chunk;
     const int64_t nchunks = (n + kChunk - 1) / kChunk;
     if (static_cast<size_t>(nchunks) > kMaxChunks) fail(LSNIF_INVALID_ARGUMENT, "too many columns in one call");
     ck(cudaMemsetAsync(w.counters, 0, kChunkCounterBytes * nchunks, st), "cudaMemsetAsync");

@@ -163,9 +163,10 @@ def test_query_stats(gmodel, oracle_teapot):
 
 
 def test_chunked_query_consistent(gmodel):
-    """> 2^23 rays spans several trace/MLP launches: results must equal the
+    """More rays than one trace/MLP launch pair takes (2^23 or 2^24 per
+    stream workspace) span several launches: results must equal the
     per-slice results bit for bit (rays are independent)."""
-    rays = W.incoherent_rays(9_000_000, gmodel.aabb, seed=9)
+    rays = W.incoherent_rays((1 << 24) + (1 << 20) + 7, gmodel.aabb, seed=9)
     t = lsnif.rays_to_tensor(rays)
     full = gmodel.query(t).cpu().numpy()
     part = torch.cat([gmodel.query(t[:1234567]), gmodel.query(t[1234567:])]).cpu().numpy()
@@ -356,10 +357,11 @@ def test_fast_path_max_hit_cap_large_launch(tmp_path, oracle_teapot):
     assert vis >= 0.999 and mat >= 0.999, (vis, mat)
 
 
-@pytest.mark.parametrize("n", [0, 1, 31, 33, 127, 129, (1 << 21) - 1, (1 << 21) + 1, (1 << 23) + 1])
+@pytest.mark.parametrize("n", [0, 1, 31, 33, 127, 129, (1 << 21) - 1, (1 << 21) + 1, (1 << 23) + 1,
+                               (1 << 24) + 1])
 def test_batch_and_chunk_boundaries(gmodel, oracle_teapot, n):
     """Ray counts at the edges of 32-ray warp batches, 128-row MLP tiles,
-    2^21-ray host staging steps and 2^23-ray launch chunks (and the empty
+    2^21-ray host staging steps and 2^23 / 2^24-ray launch chunks (and the empty
     query): every result equals the
     same rays answered inside a larger batch, bit for bit, and the pair /
     visibility flags equal the oracle's on a sample."""
