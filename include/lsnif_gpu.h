@@ -154,7 +154,11 @@ lsnif_status lsnif_model_get_info(lsnif_model model, lsnif_model_info* out);
  * fused with pair emission (renderer.cpp:165-172) and the accept rule of
  * intersect_scene (mode CLOSEST, renderer.cpp:280-301) or occluded_batch
  * (mode ANY, renderer.cpp:316-321). Rays/hits are DEVICE pointers; one
- * result per ray, in ray order. Asynchronous on `stream`. */
+ * result per ray, in ray order. Asynchronous on `stream`. Scratch is kept
+ * per (model, stream) and sized by the largest query: queries run in launch
+ * pairs of 2^24 rays (~18.8 GB of scratch for the teapot-size model) when a
+ * quarter of the free device memory holds that at the stream's first query,
+ * else 2^23 (~9.4 GB); LSNIF_CHUNK_LOG2 fixes the size. */
 lsnif_status lsnif_query(lsnif_model model, const lsnif_ray* d_rays, int64_t n, int mode,
                          lsnif_hit* d_hits, void* stream);
 
