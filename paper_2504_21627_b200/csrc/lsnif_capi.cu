@@ -292,17 +292,31 @@ struct lsnif_model_s {
     }
     Workspace& w = *slot;
     // X / meta: one region per K bin, each able to hold every row of a chunk
-    const int64_t rows = std::min<int64_t>(n, w.chunk);
-    const size_t tiles = static_cast<size_t>((rows + kTileM - 1) / kTileM);
-    if (tiles > w.x_tiles) {
+    for (;;) {
+      const int64_t rows = std::min<int64_t>(n, w.chunk);
+      const size_t tiles = static_cast<size_t>((rows + kTileM - 1) / kTileM);
+      if (tiles <= w.x_tiles) break;
       cudaFree(w.X);
       cudaFree(w.meta);
       w.X = nullptr;
       w.meta = nullptr;
-      ck(cudaMalloc(&w.X, lsnif_dev::bin_x_offset(dm.n_bins, static_cast<int64_t>(tiles))), "cudaMalloc(X)");
-      ck(cudaMalloc(&w.meta, static_cast<size_t>(dm.n_bins) * tiles * kTileM * sizeof(RowMeta)),
-         "cudaMalloc(meta)");
-      w.x_tiles = tiles;
+      w.x_tiles = 0;
+      cudaError_t e = cudaMalloc(&w.X, lsnif_dev::bin_x_offset(dm.n_bins, static_cast<int64_t>(tiles)));
+      if (e == cudaSuccess)
+        e = cudaMalloc(&w.meta, static_cast<size_t>(dm.n_bins) * tiles * kTileM * sizeof(RowMeta));
+      if (e == cudaSuccess) {
+        w.x_tiles = tiles;
+        break;
+      }
+      cudaFree(w.X);
+      w.X = nullptr;
+      w.meta = nullptr;
+      (void)cudaGetLastError();  // allocation failures are not sticky
+      if (e == cudaErrorMemoryAllocation && w.chunk > (int64_t(1) << 23) && !chunk_override()) {
+        w.chunk = int64_t(1) << 23;  // memory got tighter since pick_chunk: smaller launches
+        continue;
+      }
+      ck(e, "cudaMalloc(query workspace)");
     }
     return w;
   }

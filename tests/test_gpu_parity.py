@@ -18,6 +18,8 @@ pytestmark = pytest.mark.gpu
 from paper_2504_21627_b200 import lsnif, workloads as W  # noqa: E402
 from helpers import edge_rays  # noqa: E402
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 
 @pytest.fixture(scope="module")
 def gmodel(teapot_path):
@@ -469,3 +471,40 @@ def test_gpu_against_reference_library(gmodel, teapot_path):
     gt = {k: v.cpu().numpy() for k, v in gmodel.debug_traverse(lsnif.rays_to_tensor(rays[:20000])).items()}
     assert np.array_equal(gt["hidx"].view(np.uint32), tr["hidx"])
     assert np.array_equal(gt["feat"].view(np.uint32), tr["feat"].view(np.uint32))
+
+
+def test_workspace_falls_back_when_memory_tightens(teapot_path):
+    """A stream whose first query picked 2^24-ray launch pairs (plenty of free
+    HBM) and whose next large query no longer fits that workspace drops to
+    2^23-ray launches instead of failing; results stay bit-identical to
+    per-slice queries. Runs in a subprocess: it holds most of the GPU."""
+    import subprocess
+    import sys
+    code = f"""
+import sys, numpy as np, torch
+sys.path.insert(0, {ROOT!r})
+from paper_2504_21627_b200 import lsnif, workloads as W
+gm = lsnif.GpuModel({teapot_path!r}, 0)
+small = lsnif.rays_to_tensor(W.camera_rays(64, 64), "cuda")
+gm.query(small)  # the stream's workspace: launch size picked with the GPU nearly empty
+rays = lsnif.rays_to_tensor(W.incoherent_rays((1 << 24) + 5, gm.aabb, seed=5), "cuda")
+side = torch.cuda.Stream()  # the reference slices on another stream (its own workspace)
+side.wait_stream(torch.cuda.current_stream())
+ref = torch.cat([gm.query(rays[:3_000_001], stream=side), gm.query(rays[3_000_001:], stream=side)])
+torch.cuda.synchronize()
+free, _ = torch.cuda.mem_get_info()
+hog = torch.empty(max(0, free - (14 << 30)), dtype=torch.uint8, device="cuda")
+gm.profile_read(reset=True, stream="all")
+out = gm.query(rays)
+torch.cuda.synchronize()
+launches = gm.profile_read(reset=True, stream="all")["trace_launches"]
+assert torch.equal(out, ref)
+assert launches == 3, launches  # 2^23-ray launch pairs after the fallback (2 at 2^24)
+print("fallback ok", free >> 30)
+"""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if os.environ.get("LSNIF_CHUNK_LOG2"):
+        pytest.skip("launch size fixed by LSNIF_CHUNK_LOG2")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "fallback ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
